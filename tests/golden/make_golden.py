@@ -1,0 +1,225 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE.
+
+Run in the build container (needs /root/reference):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Each ``<name>.npz`` holds
+  * the problem exactly as the reference built it (CSR arrays of G, the
+    collapse and expectation operators, psi0, grid, ODE config and the
+    reference's own automatic first step ``h0``, read back from
+    ``OdeSolver.h``, ode.py:199-203, 247-252);
+  * per-trajectory outputs of ``mcwf.trajectory.run_single_trajectory``
+    (trajectory.py:190-250) under per-trajectory streams from
+    ``oracle/streams.py`` (philox / lfsr113 / scripted): the expectation
+    series, the jump log (t*, channel), the number of draws consumed and
+    snapshots of psi at selected grid points (captured by wrapping the
+    module-global ``record_expectation``, which ``record`` looks up at call
+    time, trajectory.py:206-214).
+
+The fixtures pin the C oracle (tests/test_oracle_golden.py) and the device
+kernels (tests/test_gpu_parity.py).  Nothing on the GPU box reads
+/root/reference; it only reads these files.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, HERE)
+
+import ref_configs  # noqa: E402  (puts /root/reference/pkg/src on sys.path)
+import mcwf  # noqa: E402
+from mcwf import rng as ref_rng  # noqa: E402
+from mcwf import trajectory as ref_traj  # noqa: E402
+from mcwf.linalg import to_csr  # noqa: E402
+from mcwf.ode import OdeConfig, OdeFailure, OdeSolver  # noqa: E402
+from mcwf.operators import OperatorSet, fock, sigma_minus, sigma_x, sigma_z  # noqa: E402
+from mcwf.problems import build_photon, build_trilinear, build_unitary  # noqa: E402
+from mcwf.trajectory import QuantumProblem, RunOptions  # noqa: E402
+
+from oracle.streams import (Lfsr113Stream, PhiloxStream, ScriptedStream,  # noqa: E402
+                            lfsr113_derive)
+
+SEED = 987654321  # reference DEFAULT_SEED, rng.py:25
+
+
+def problem_arrays(p: QuantumProblem) -> dict:
+    out = {"dim": p.dim, "t_from": p.t_from, "t_to": p.t_to, "n_steps": p.n_steps,
+           "rtol": p.ode.rtol, "atol": p.ode.atol, "max_order": p.ode.max_order,
+           "max_steps": p.ode.max_steps,
+           "initial_step": np.nan if p.ode.initial_step is None else p.ode.initial_step,
+           "psi0": p.psi0, "times": p.time_grid(),
+           "n_collapse": len(p.collapse_csr), "n_expect": len(p.expect_csr)}
+    g = p.generator.g
+    out.update(g_row_ptr=g.row_ptr, g_col_ind=g.col_ind, g_values=g.values)
+    for tag, ops in (("c", p.collapse_csr), ("e", p.expect_csr)):
+        for i, m in enumerate(ops):
+            out[f"{tag}{i}_row_ptr"] = m.row_ptr
+            out[f"{tag}{i}_col_ind"] = m.col_ind
+            out[f"{tag}{i}_values"] = m.values
+    out["h0"] = OdeSolver(p.ode, g, t0=p.t_from, y0=p.psi0.copy()).h
+    return out
+
+
+class _PsiCapture:
+    def __init__(self, dim, n_pts, keep):
+        self.keep = set(int(g) for g in keep)
+        self.buf = {}
+        self.gi = None
+        self.orig = ref_traj.record_expectation
+
+    def __enter__(self):
+        cap = self
+        orig = self.orig
+
+        def wrapped(psi, e):
+            cap.calls.append(np.array(psi, copy=True))
+            return orig(psi, e)
+
+        self.calls = []
+        ref_traj.record_expectation = wrapped
+        return self
+
+    def __exit__(self, *exc):
+        ref_traj.record_expectation = self.orig
+
+
+def run_sample(p, kind, indices, psi_points, n_expect, script=None):
+    n_pts = p.n_steps + 1
+    vals, jcount, jt, jidx, ndraws, psis = [], [], [], [], [], []
+    for k in indices:
+        if kind == "philox":
+            st = PhiloxStream(SEED, k)
+        elif kind == "lfsr113":
+            st = Lfsr113Stream(SEED, k)
+        else:
+            st = ScriptedStream(script[k], 0.999999)
+        cap = _PsiCapture(p.dim, n_pts, psi_points)
+        with cap:
+            res, st2 = ref_traj.run_single_trajectory(p, st)
+        # record() calls record_expectation once per expectation operator per
+        # grid point, in grid order
+        per_point = cap.calls[::n_expect]
+        assert len(per_point) == n_pts
+        psis.append(np.stack([per_point[g] for g in psi_points]) if len(psi_points) else
+                    np.zeros((0, p.dim), complex))
+        vals.append(res.values)
+        jumps = res.jumps or []
+        jcount.append(len(jumps))
+        jt.extend(t for t, _ in jumps)
+        jidx.extend(i for _, i in jumps)
+        ndraws.append(st.n if hasattr(st, "n") else 1 + 2 * len(jumps))
+    return {"kind": kind, "traj": np.asarray(indices, np.int64),
+            "values": np.stack(vals), "jump_count": np.asarray(jcount, np.int64),
+            "jump_t": np.asarray(jt, float), "jump_idx": np.asarray(jidx, np.int64),
+            "n_draws": np.asarray(ndraws, np.int64),
+            "psi_points": np.asarray(psi_points, np.int64), "psi": np.stack(psis)}
+
+
+def save(name, p, samples, extra=None):
+    arrs = {f"prob_{k}": np.asarray(v) for k, v in problem_arrays(p).items()}
+    arrs["seed"] = np.uint64(SEED)
+    for s in samples:
+        tag = s["kind"]
+        for k, v in s.items():
+            if k != "kind":
+                arrs[f"{tag}_{k}"] = np.asarray(v)
+    arrs["kinds"] = np.array([s["kind"] for s in samples])
+    if extra:
+        arrs.update(extra)
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrs)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KB)")
+
+
+def with_log(p):
+    return dataclasses.replace(p, options=RunOptions(log_jumps=True))
+
+
+def main():
+    t0 = time.time()
+    plan = {  # name: (philox indices, lfsr indices, psi grid points)
+        "c1": (list(range(64)), list(range(16)), list(range(0, 201, 5))),
+        "c2": (list(range(12)), list(range(4)), list(range(0, 301, 10))),
+        "c3": (list(range(6)), list(range(2)), list(range(0, 501, 25))),
+        "c4": (list(range(4)), [0], list(range(0, 101, 20))),
+        "c5": ([0, 1], [0], list(range(0, 401, 80))),
+    }
+    for name, (ph, lf, pts) in plan.items():
+        p = ref_configs.CONFIGS[name]()
+        n_e = len(p.expect_csr)
+        samples = [run_sample(p, "philox", ph, pts, n_e),
+                   run_sample(p, "lfsr113", lf, pts[:4], n_e)]
+        save(name, p, samples)
+        print(f"  {name}: {time.time() - t0:.1f}s")
+
+    # reference unit-test scenarios (tests/test_trajectory.py) ----------------
+    decay = lambda t_to, n_steps, rtol=1e-8: QuantumProblem.from_operators(  # noqa: E731
+        OperatorSet(np.zeros((2, 2), complex), (sigma_minus(),), (sigma_z(),)),
+        fock(2, 1), 0.0, t_to, n_steps, ode=OdeConfig(rtol=rtol, atol=1e-12),
+        options=RunOptions(log_jumps=True))
+    p = decay(12.0, 12)
+    scripts = {0: [0.5, 0.3, 0.9999999]}
+    save("decay_forced_jump", p, [run_sample(p, "scripted", [0], range(13), 1, scripts)])
+    p = decay(1.0, 10)
+    scripts = {0: [np.exp(-1.0) / 2]}
+    save("decay_no_jump", p, [run_sample(p, "scripted", [0], range(11), 1, scripts)])
+    p = decay(12.0, 12)
+    save("decay_streams", p, [run_sample(p, "philox", list(range(32)), [], 1),
+                              run_sample(p, "lfsr113", list(range(16)), [], 1)])
+
+    omega = 2 * np.pi / 10
+    rabi = QuantumProblem.from_operators(
+        OperatorSet(omega * sigma_x(), (), (sigma_z(),)), fock(2, 0), 0.0, 10.0, 100,
+        ode=OdeConfig(rtol=1e-8, atol=1e-12), options=RunOptions(log_jumps=True))
+    save("rabi_closed", rabi, [run_sample(rabi, "philox", [0], list(range(101)), 1)])
+    rabi_c = QuantumProblem.from_operators(
+        OperatorSet(omega * sigma_x(), (0.05 * sigma_x(),), (sigma_z(),)), fock(2, 0),
+        0.0, 10.0, 100, ode=OdeConfig(rtol=1e-8, atol=1e-12),
+        options=RunOptions(log_jumps=True))
+    save("rabi_collapse", rabi_c, [run_sample(rabi_c, "philox", list(range(32)), [], 1)])
+
+    for name, builder, nph in (("photon", build_photon, 48), ("unitary", build_unitary, 32),
+                               ("trilinear", build_trilinear, 2)):
+        p = with_log(builder())
+        save(name, p, [run_sample(p, "philox", list(range(nph)), [0, p.n_steps // 2],
+                                  len(p.expect_csr))])
+
+    # failure scenarios: the exact exception text the boundary must mirror
+    msgs = {}
+    p = dataclasses.replace(ref_configs.c1(), ode=OdeConfig(rtol=1e-8, atol=1e-10, max_steps=1))
+    try:
+        ref_traj.run_single_trajectory(p, PhiloxStream(SEED, 0))
+    except OdeFailure as exc:
+        msgs["max_steps_msg"] = np.array(str(exc))
+        msgs["max_steps_istate"] = np.int64(exc.istate)
+    save("c1_max_steps", p, [], msgs)
+
+    # LFSR113 stream bits: derive_stream(seed, k) words and first 64 draws
+    words, draws = [], []
+    for k in range(8):
+        st = ref_rng.derive_stream(SEED, k)
+        words.append((st.z1, st.z2, st.z3, st.z4))
+        assert tuple(lfsr113_derive(SEED, k)) == words[-1]
+        row = []
+        for _ in range(64):
+            u, st = st.next_u01()
+            row.append(u)
+        draws.append(row)
+    np.savez_compressed(os.path.join(HERE, "lfsr113_streams.npz"),
+                        seed=np.uint64(SEED), words=np.asarray(words, np.uint64),
+                        draws=np.asarray(draws))
+    print(f"done in {time.time() - t0:.1f}s  (mcwf {mcwf.__version__})")
+
+
+if __name__ == "__main__":
+    main()

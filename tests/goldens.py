@@ -1,0 +1,75 @@
+"""Load tests/golden/*.npz (made by tests/golden/make_golden.py from the
+reference) into this package's problem types plus the reference outputs."""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_1810_03047_b200.csr import CsrMatrix
+from paper_1810_03047_b200.problem import OdeConfig, QuantumProblem, RunOptions
+from paper_1810_03047_b200.qops import EffectiveGenerator
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SEED = 987654321
+
+
+@dataclass
+class Sample:
+    kind: str
+    traj: np.ndarray
+    values: np.ndarray
+    jump_count: np.ndarray
+    jump_t: list
+    jump_idx: list
+    n_draws: np.ndarray
+    psi_points: np.ndarray
+    psi: np.ndarray
+
+
+@dataclass
+class Golden:
+    name: str
+    problem: QuantumProblem
+    h0: float
+    samples: dict
+    raw: dict
+
+
+def _csr(z, prefix, n):
+    return CsrMatrix(n, z[f"{prefix}_row_ptr"], z[f"{prefix}_col_ind"], z[f"{prefix}_values"])
+
+
+def load(name: str) -> Golden:
+    z = dict(np.load(os.path.join(GOLDEN_DIR, f"{name}.npz"), allow_pickle=False))
+    n = int(z["prob_dim"])
+    init = float(z["prob_initial_step"])
+    ode = OdeConfig(rtol=float(z["prob_rtol"]), atol=float(z["prob_atol"]),
+                    max_order=int(z["prob_max_order"]), max_steps=int(z["prob_max_steps"]),
+                    initial_step=None if np.isnan(init) else init)
+    p = QuantumProblem(
+        generator=EffectiveGenerator(CsrMatrix(n, z["prob_g_row_ptr"], z["prob_g_col_ind"],
+                                               z["prob_g_values"])),
+        collapse_csr=tuple(_csr(z, f"prob_c{i}", n) for i in range(int(z["prob_n_collapse"]))),
+        expect_csr=tuple(_csr(z, f"prob_e{i}", n) for i in range(int(z["prob_n_expect"]))),
+        psi0=z["prob_psi0"], t_from=float(z["prob_t_from"]), t_to=float(z["prob_t_to"]),
+        n_steps=int(z["prob_n_steps"]), ode=ode, options=RunOptions(log_jumps=True))
+    samples = {}
+    for kind in [str(k) for k in z.get("kinds", [])]:
+        counts = z[f"{kind}_jump_count"]
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        jt = [z[f"{kind}_jump_t"][offs[i]:offs[i + 1]] for i in range(len(counts))]
+        ji = [z[f"{kind}_jump_idx"][offs[i]:offs[i + 1]] for i in range(len(counts))]
+        samples[kind] = Sample(kind, z[f"{kind}_traj"], z[f"{kind}_values"], counts, jt, ji,
+                               z[f"{kind}_n_draws"], z[f"{kind}_psi_points"], z[f"{kind}_psi"])
+    return Golden(name, p, float(z["prob_h0"]), samples, z)
+
+
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
+SCENARIOS = ("decay_forced_jump", "decay_no_jump", "decay_streams", "rabi_closed",
+             "rabi_collapse", "photon", "unitary", "trilinear")
+
+SCRIPTS = {"decay_forced_jump": [[0.5, 0.3, 0.9999999]],
+           "decay_no_jump": [[float(np.exp(-1.0) / 2)]]}
