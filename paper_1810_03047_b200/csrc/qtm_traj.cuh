@@ -1,0 +1,739 @@
+// qtm_traj.cuh -- persistent sm_100a kernel that integrates whole quantum
+// trajectories on chip.
+//
+// Mapping.  One CTA owns one trajectory at a time; NT threads each own E
+// state components (component i = tid + NT*e, so shared-memory traffic is
+// conflict-free).  The Nordsieck history z[0..q] lives in REGISTERS for rows
+// j < RREG (rows >= RREG, reached only when the order climbs past the
+// variant's budget, spill to a per-CTA global scratch).  Every thread
+// evaluates the scalar controller (t, h, q, crate, ialth, nef, ncf, r, ...)
+// redundantly from bitwise-identical block reductions, so control flow is
+// CTA-uniform with no broadcasts.  The CTA pulls the next trajectory index
+// from a global atomic counter when it finishes one (dynamic load balance
+// for the heavy-tailed step counts); outputs land in per-trajectory slots,
+// so results do not depend on scheduling.
+//
+// Reference behaviour reproduced per attempt:
+//   predict / corrector / error test / commit ..... _kernels.py:117-192
+//   retry loop, rejects, restarts ................. ode.py:261-329
+//   order & step control .......................... ode.py:441-466
+//   jump test, bisection, collapse, cold restart .. trajectory.py:133-182, 216-246
+//   expectation recording ......................... trajectory.py:122-130, 206-214
+// Differences from the reference are rounding-level only: block reductions
+// are tree sums (the reference sums sequentially), the predicted history is
+// undone in place on a rejected attempt instead of kept in a second copy,
+// and hypot/pow come from CUDA's libdevice.
+#pragma once
+#include <cstdint>
+
+#include "qtm_rng.cuh"
+
+namespace qtm {
+
+constexpr int LROWS = 13;
+constexpr int MAXOPS = 32;
+constexpr int KRED = 4;  // values carried by one block reduction
+constexpr int NSTATS = 16;
+
+enum Status : int {
+    kOk = 0, kErrMaxSteps = -1, kErrRepeatedErrTest = -4, kErrStepCollapse = -5,
+    kErrCorrector = -6, kErrBracket = -10, kErrNoSupport = -11, kErrZeroVector = -12,
+};
+
+enum Stat : int {
+    sAttempts = 0, sSteps, sCorrFail, sErrReject, sNfe, sCorrIters, sJumps, sBisect, sSumQ,
+    sOrderUp, sOrderDown, sDraws, sSumQQ1, sOverflow,
+};
+
+// one compiled kernel configuration (see build.py VARIANTS)
+struct VariantDesc {
+    int threads, comps, reg_rows, min_blocks, auto_upto;
+    size_t smem;
+    const void* fn;
+};
+
+struct DevCsr {
+    const int* rp;
+    const int* ci;
+    const double2* v;
+};
+
+struct DevProblem {
+    int d, nc, ne, n_pts, max_order;
+    long long max_steps;
+    double t_from, t_to, rtol, atol, h0_first;
+    DevCsr g;
+    DevCsr c[MAXOPS];
+    DevCsr e[MAXOPS];
+    const double2* psi0;
+    const double* times;
+    double l[LROWS][LROWS];
+    double tau1[LROWS], tau2[LROWS], tau3[LROWS];
+};
+
+struct RunParams {
+    uint64_t seed;
+    long long traj_begin, n_traj;
+    int stream_kind;
+    const double* script;
+    const long long* script_len;
+    long long script_stride;
+    double script_fallback;
+    double* values;          // [n_traj][ne][n_pts]
+    long long* stats;        // [n_traj][NSTATS]
+    int* status;             // [n_traj]
+    double* err;             // [n_traj][4]: t, h, aux0, aux1   (aux2 = r in err_r)
+    double* err_r;           // [n_traj]
+    long long* jump_count;   // [n_traj]
+    double* jump_t;          // [n_traj][max_jumps]
+    int* jump_idx;           // [n_traj][max_jumps]
+    long long max_jumps;
+    double2* zovf;           // [gridDim.x][LROWS-RREG][NT*E]
+    unsigned long long* counter;
+    unsigned long long* first_fail;  // atomicMin over failing rows
+};
+
+// ---------------------------------------------------------------- helpers
+// The reference's numba kernels are compiled without fast-math, so no a*b+c
+// is fused; this file is built with -fmad=false to keep the same rounding.
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then
+// accumulated (reference _kernels.py:150-154, numba complex_mul).
+__device__ __forceinline__ double2 row_dot(const DevCsr& m, int i, const double2* __restrict__ x) {
+    double sr = 0.0, si = 0.0;
+    const int b = __ldg(m.rp + i), en = __ldg(m.rp + i + 1);
+    for (int j = b; j < en; ++j) {
+        const double2 v = __ldg(m.v + j);
+        const double2 xv = x[__ldg(m.ci + j)];
+        sr = sr + (v.x * xv.x - v.y * xv.y);
+        si = si + (v.x * xv.y + v.y * xv.x);
+    }
+    return make_double2(sr, si);
+}
+
+// Bitwise-identical sums on every thread of the CTA: xor-butterfly inside
+// each warp (a+b == b+a at every level, so all lanes agree), lane 0 of every
+// warp publishes its partial, then every warp loads the NW partials one per
+// lane and runs the same butterfly -- identical data and order in every warp.
+// Double-buffered scratch => one barrier per reduction.
+template <int NT, int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& phase) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], m);
+    }
+    if constexpr (NT > 32) {
+        constexpr int NW = NT / 32;
+        double* buf = red + phase * (KRED * NW);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) buf[k * NW + warp] = v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = lane < NW ? buf[k * NW + lane] : 0.0;
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+            v[k] = s;
+        }
+        phase ^= 1;
+    }
+}
+
+
+// ------------------------------------------------ Nordsieck history helpers
+// Rows j < RREG are a register array (static indices after unrolling, with
+// uniform runtime predicates on q); rows j >= RREG live in the thread's
+// overflow column ovf[e][(j - RREG) * DP] and are walked by plain runtime
+// loops, so the register path carries no overflow code.
+template <int RREG, int E, int DP>
+struct Hist {
+    using Z = double2[RREG][E];
+    using O = double2* [E];
+
+    // zp = Pascal(z) in place, passes r = 0..q-1, j = q-1 down to r
+    // (_kernels.py:133-137)
+    __device__ __forceinline__ static void predict(Z& z, O& ovf, int q) {
+        for (int r = 0; r < q; ++r) {
+            for (int j = q - 1; j >= (r > RREG ? r : RREG); --j) {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    ovf[e][(j - RREG) * DP] = cadd(ovf[e][(j - RREG) * DP], ovf[e][(j + 1 - RREG) * DP]);
+            }
+            if (RREG - 1 >= r && RREG - 1 < q) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[RREG - 1][e] = cadd(z[RREG - 1][e], ovf[e][0]);
+            }
+#pragma unroll
+            for (int j = RREG - 2; j >= 0; --j) {
+                if (j >= r && j < q) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) z[j][e] = cadd(z[j][e], z[j + 1][e]);
+                }
+            }
+        }
+    }
+
+    // inverse of predict (rejected attempt): passes r = q-1..0, j = r..q-1
+    __device__ __forceinline__ static void undo(Z& z, O& ovf, int q) {
+        for (int r = q - 1; r >= 0; --r) {
+#pragma unroll
+            for (int j = 0; j < RREG - 1; ++j) {
+                if (j >= r && j < q) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) z[j][e] = csub(z[j][e], z[j + 1][e]);
+                }
+            }
+            if (RREG - 1 >= r && RREG - 1 < q) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[RREG - 1][e] = csub(z[RREG - 1][e], ovf[e][0]);
+            }
+            for (int j = (r > RREG ? r : RREG); j < q; ++j) {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    ovf[e][(j - RREG) * DP] = csub(ovf[e][(j - RREG) * DP], ovf[e][(j + 1 - RREG) * DP]);
+            }
+        }
+    }
+
+    // z[j] *= ratio^j, j = 1..q, ratio^j by repeated multiplication
+    // (nordsieck_rescale, _kernels.py:107-114)
+    __device__ __forceinline__ static void rescale(Z& z, O& ovf, int q, double ratio) {
+        double f = 1.0;
+#pragma unroll
+        for (int j = 1; j < RREG; ++j) {
+            if (j <= q) {
+                f *= ratio;
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[j][e] = cscale(f, z[j][e]);
+            }
+        }
+        for (int j = RREG; j <= q; ++j) {
+            f *= ratio;
+#pragma unroll
+            for (int e = 0; e < E; ++e) ovf[e][(j - RREG) * DP] = cscale(f, ovf[e][(j - RREG) * DP]);
+        }
+    }
+
+    // z[j] += l_j e, j = 0..q (_kernels.py:187-191)
+    __device__ __forceinline__ static void commit(Z& z, O& ovf, int q, const double* l,
+                                                  const double2 (&ev)[E]) {
+#pragma unroll
+        for (int j = 0; j < RREG; ++j) {
+            if (j <= q) {
+                const double lj = l[j];
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[j][e] = cadd(z[j][e], cscale(lj, ev[e]));
+            }
+        }
+        for (int j = RREG; j <= q; ++j) {
+            const double lj = l[j];
+#pragma unroll
+            for (int e = 0; e < E; ++e) ovf[e][(j - RREG) * DP] = cadd(ovf[e][(j - RREG) * DP], cscale(lj, ev[e]));
+        }
+    }
+
+    __device__ __forceinline__ static double2 row(const Z& z, O& ovf, int j, int e) {
+        if (j >= RREG) return ovf[e][(j - RREG) * DP];
+        double2 out = z[0][e];
+#pragma unroll
+        for (int jj = 1; jj < RREG; ++jj) if (jj == j) out = z[jj][e];
+        return out;
+    }
+
+    __device__ __forceinline__ static void set_row(Z& z, O& ovf, int j, int e, double2 v) {
+        if (j >= RREG) { ovf[e][(j - RREG) * DP] = v; return; }
+#pragma unroll
+        for (int jj = 0; jj < RREG; ++jj) if (jj == j) z[jj][e] = v;
+    }
+
+    // psi(s) = Horner over rows q..0 (nordsieck_eval, _kernels.py:61-69)
+    __device__ __forceinline__ static void horner(const Z& z, O& ovf, int q, double s, double2 (&out)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = row(z, ovf, q, e);
+        for (int j = q - 1; j >= RREG; --j) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[e] = cadd(cscale(s, out[e]), ovf[e][(j - RREG) * DP]);
+        }
+#pragma unroll
+        for (int j = RREG - 1; j >= 0; --j) {
+            if (j < q) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) out[e] = cadd(cscale(s, out[e]), z[j][e]);
+            }
+        }
+    }
+};
+
+// ------------------------------------------------------------- the kernel
+template <int NT, int E, int RREG>
+struct TrajKernel {
+    static constexpr int DP = NT * E;  // padded state length
+    static constexpr int NW = NT / 32;
+
+    static constexpr size_t smem_bytes() {
+        return sizeof(double2) * (size_t)DP * 4 + sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1);
+    }
+};
+
+// Row access: rows < RREG are register arrays indexed by compile-time j
+// (every loop over j is fully unrolled), rows >= RREG live in the CTA's
+// overflow scratch.
+#define STAT(which, amount) do { if (tid == 0) s_stats[which] += (amount); } while (0)
+
+template <int NT, int E, int RREG, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R) {
+    constexpr int DP = NT * E;
+    using H = Hist<RREG, E, DP>;
+    extern __shared__ double2 smem[];
+    // gath[2][DP]: double-buffered gather buffers; gath[gbuf] is the most
+    //              recently published vector (the corrector iterate lives here)
+    // ebuf[2][DP]: corrector term e of the current attempt / of the previous
+    //              accepted step (e_prev); "e_prev = e.copy()" is a flip
+    double2* const gath = smem;
+    double2* const ebuf = smem + 2 * DP;
+    double* const red = reinterpret_cast<double*>(smem + 4 * DP);
+    __shared__ long long s_row;
+    __shared__ long long s_stats[NSTATS];
+    __shared__ Stream s_stream;
+    __shared__ double s_draw;
+
+    const int tid = threadIdx.x;
+    const int d = P.d;
+    const int npts = P.n_pts;
+    int ii[E];
+    bool act[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { ii[e] = tid + NT * e; act[e] = ii[e] < d; }
+    double2* ovf[E];  // this thread's overflow column, row j at ovf[e][(j - RREG) * DP]
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        ovf[e] = (RREG < LROWS) ? R.zovf + (size_t)blockIdx.x * (LROWS - RREG) * DP + ii[e] : nullptr;
+
+    int gbuf = 0, rphase = 0, ecur = 0;
+
+    for (;;) {
+        if (tid == 0) s_row = (long long)atomicAdd(R.counter, 1ull);
+        __syncthreads();
+        const long long row = s_row;
+        if (row >= R.n_traj) break;
+        if (tid < NSTATS) s_stats[tid] = 0;
+        if (tid == 0)
+            s_stream.init(R.stream_kind, R.seed, (uint64_t)(R.traj_begin + row),
+                          R.script ? R.script + row * R.script_stride : nullptr,
+                          R.script_len ? R.script_len[row] : 0, R.script_fallback);
+        __syncthreads();
+
+        long long njumps = 0;
+        int rc = kOk;
+
+        double2 z[RREG][E];  // Nordsieck history rows 0..RREG-1 (registers)
+        double w[E];         // error weights 1/(atol + rtol |z0_i|)
+        double t, t_lo, h, crate;
+        int q, ialth;
+        bool has_eprev;
+
+// publish x[E] as the next gather buffer (write, barrier); yields `xs`
+#define GATHER(xsrc, xs)                                                     \
+    double2* const xs = gath + (gbuf ^ 1) * DP;                              \
+    _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) xs[ii[e]] = (xsrc)[e]; \
+    __syncthreads();                                                         \
+    gbuf ^= 1;
+
+// Horner evaluation of the history polynomial at s into out[E]
+#define HORNER(s_, out) H::horner(z, ovf, q, (s_), out)
+
+// z[j] *= ratio^j for j = 1..q, h *= ratio (nordsieck_rescale + _rescale)
+#define RESCALE(ratio_)                                                      \
+    do {                                                                     \
+        const double rr__ = (ratio_);                                        \
+        H::rescale(z, ovf, q, rr__);                                         \
+        h *= rr__;                                                           \
+        has_eprev = false;                                                   \
+        ialth = q + 1;                                                       \
+    } while (0)
+
+#define FAIL4(code_, a_, b_, c_, d_)                                         \
+    do {                                                                     \
+        rc = (code_);                                                        \
+        if (tid == 0) {                                                      \
+            double* eo__ = R.err + (size_t)row * 4;                          \
+            eo__[0] = (a_); eo__[1] = (b_); eo__[2] = (c_); eo__[3] = (d_);  \
+        }                                                                    \
+        goto traj_done;                                                      \
+    } while (0)
+#define FAIL(code_) FAIL4(code_, t, h, 0.0, 0.0)
+
+// one uniform draw, evaluated by thread 0 and broadcast
+#define DRAW(var)                                                            \
+    do {                                                                     \
+        __syncthreads();                                                     \
+        if (tid == 0) s_draw = s_stream.next();                              \
+        __syncthreads();                                                     \
+        var = s_draw;                                                        \
+    } while (0)
+
+        // ---- record(gi) of the state in `psi` (trajectory.py:122-130, 206-214)
+#define RECORD(psi, gi_)                                                     \
+    do {                                                                     \
+        GATHER(psi, xs__);                                                   \
+        double nrm__ = 0.0;                                                  \
+        _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) nrm__ += cabs2(psi[e]); \
+        for (int k0 = 0; k0 < P.ne; k0 += KRED - 1) {                        \
+            double v__[KRED] = {0.0, 0.0, 0.0, nrm__};                       \
+            for (int kk = 0; kk < KRED - 1; ++kk) {                          \
+                const int k = k0 + kk;                                       \
+                if (k < P.ne) {                                              \
+                    _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) { \
+                        const double2 s = row_dot(P.e[k], ii[e], xs__);      \
+                        v__[kk] += psi[e].x * s.x - (-psi[e].y) * s.y;       \
+                    }                                                        \
+                }                                                            \
+            }                                                                \
+            block_sum<NT, KRED>(v__, red, rphase);                           \
+            if (v__[KRED - 1] == 0.0) FAIL(kErrZeroVector);                  \
+            if (tid == 0) {                                                  \
+                double* vals__ = R.values + ((size_t)row * P.ne + k0) * npts + (gi_); \
+                for (int kk = 0; kk < KRED - 1; ++kk)                        \
+                    if (k0 + kk < P.ne) vals__[(size_t)kk * npts] = v__[kk] / v__[KRED - 1]; \
+            }                                                                \
+        }                                                                    \
+    } while (0)
+
+        // ---- cold start of the solver at (t0, y0[E]) with step h0 (ode.py:164-217)
+#define COLD_START(t0_, y0, h0_)                                             \
+    do {                                                                     \
+        t = (t0_); t_lo = t; q = 1; h = (h0_);                               \
+        GATHER(y0, xs__);                                                    \
+        STAT(sNfe, 1);                                                       \
+        _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
+            const double2 f__ = act[e] ? row_dot(P.g, ii[e], xs__) : make_double2(0.0, 0.0); \
+            z[0][e] = (y0)[e];                                               \
+            z[1][e] = cscale(h, f__);                                        \
+            _Pragma("unroll") for (int j = 2; j < RREG; ++j) z[j][e] = make_double2(0.0, 0.0); \
+            w[e] = act[e] ? 1.0 / (P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
+        }                                                                    \
+        crate = 0.7; ialth = 2; has_eprev = false;                           \
+    } while (0)
+
+        t = P.t_from;
+        h = P.h0_first;
+        {
+            double2 psi[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) psi[e] = act[e] ? P.psi0[ii[e]] : make_double2(0.0, 0.0);
+            RECORD(psi, 0);  // record(0) from psi0
+            double r;
+            DRAW(r);
+            COLD_START(P.t_from, psi, P.h0_first);
+            int gi = 1;
+            long long steps_in_segment = 0;
+
+            while (gi < npts) {
+                // ================= OdeSolver.step() (ode.py:261-312) =================
+                int nef = 0, ncf = 0;
+                double est = 0.0, nrm2 = 0.0;
+                for (;;) {
+                    if (t + h == t) FAIL(kErrStepCollapse);
+                    STAT(sAttempts, 1);
+                    STAT(sSumQ, q);
+                    STAT(sSumQQ1, q * (q + 1));
+                    if (q + 1 > RREG) STAT(sOverflow, 1);
+                    // predict: in-place Pascal triangle (_kernels.py:133-137)
+                    H::predict(z, ovf, q);
+                    // functional corrector (_kernels.py:139-174).  The iterate
+                    // lives in the gather buffers: iteration m reads gath[gbuf]
+                    // and writes its update into gath[gbuf^1], which the
+                    // reduction barrier then publishes for iteration m+1.
+                    const double l0 = P.l[q][0];
+                    const double conit = 0.5 / (q + 2);
+                    bool converged = false;
+                    double delp = 0.0, del = 0.0, acc_e = 0.0;
+                    {
+                        double2 y0p[E];
+#pragma unroll
+                        for (int e = 0; e < E; ++e) y0p[e] = z[0][e];
+                        GATHER(y0p, xs0);
+                    }
+                    double2* const ecurp = ebuf + ecur * DP;
+                    for (int m = 0; m < 3; ++m) {
+                        const double2* const cur = gath + gbuf * DP;
+                        double2* const nxt = gath + (gbuf ^ 1) * DP;
+                        STAT(sNfe, 1);
+                        STAT(sCorrIters, 1);
+                        double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            if (act[e]) {
+                                const double2 f = row_dot(P.g, ii[e], cur);
+                                const double2 z1 = z[1][e], z0 = z[0][e];
+                                const double2 ei = csub(cscale(h, f), z1);
+                                const double2 yn = cadd(z0, cscale(l0, ei));
+                                const double2 dd = csub(yn, cur[ii[e]]);
+                                v[0] += cabs2(dd) * w[e] * w[e];
+                                v[1] += cabs2(ei) * w[e] * w[e];
+                                v[2] += cabs2(yn);
+                                nxt[ii[e]] = yn;
+                                ecurp[ii[e]] = ei;
+                            }
+                        }
+                        block_sum<NT, 3>(v, red, rphase);
+                        if constexpr (NT == 32) __syncwarp();
+                        gbuf ^= 1;
+                        del = sqrt(v[0] / (double)d);
+                        acc_e = v[1];
+                        nrm2 = v[2];
+                        if (m > 0) {
+                            const double a = 0.2 * crate, b = del / delp;
+                            crate = b > a ? b : a;
+                        }
+                        const double c15 = 1.5 * crate;
+                        if (del * (c15 < 1.0 ? c15 : 1.0) <= conit) { converged = true; break; }
+                        if (m > 0 && del > 2.0 * delp) break;
+                        delp = del;
+                    }
+                    if (converged) {
+                        est = sqrt(acc_e / (double)d) / P.tau2[q];
+                        if (!(est > 1.0)) {
+                            // commit zp[j] += l_j e (_kernels.py:187-191)
+                            double2 evr[E];
+#pragma unroll
+                            for (int e = 0; e < E; ++e) evr[e] = act[e] ? ecurp[ii[e]] : make_double2(0.0, 0.0);
+                            H::commit(z, ovf, q, P.l[q], evr);
+                            break;  // accepted
+                        }
+                    }
+                    // rejected attempt: restore the un-predicted history
+                    H::undo(z, ovf, q);
+                    if (!converged) {
+                        STAT(sCorrFail, 1);
+                        if (++ncf >= 10) FAIL(kErrCorrector);
+                        RESCALE(0.25);
+                        continue;
+                    }
+                    STAT(sErrReject, 1);
+                    if (++nef >= 10) FAIL(kErrRepeatedErrTest);
+                    if (nef >= 3) {
+                        // _restart_order_one(0.1), ode.py:314-323
+                        q = 1;
+                        h *= 0.1;
+                        double2 y0c[E];
+#pragma unroll
+                        for (int e = 0; e < E; ++e) y0c[e] = z[0][e];
+                        GATHER(y0c, xs);
+                        STAT(sNfe, 1);
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const double2 f = act[e] ? row_dot(P.g, ii[e], xs) : make_double2(0.0, 0.0);
+                            z[1][e] = cscale(h, f);
+                        }
+                        has_eprev = false;
+                        ialth = q + 1;
+                    } else {
+                        const double rr = 1.0 / (1.2 * pow(est, 1.0 / (q + 1)) + 1e-6);
+                        const double m1 = 0.9 < rr ? 0.9 : rr;
+                        RESCALE(m1 > 0.1 ? m1 : 0.1);
+                    }
+                }
+                // accepted step bookkeeping (ode.py:281-292)
+                t_lo = t;
+                t += h;
+                STAT(sSteps, 1);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const double2 z0 = z[0][e];
+                    w[e] = act[e] ? 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
+                }
+                ialth -= 1;
+                if (ialth == 0) {
+                    // _order_step_control (ode.py:441-466)
+                    const double r_same = 1.0 / (1.2 * pow(est, 1.0 / (q + 1)) + 1e-6);
+                    const bool need_d = q > 1;
+                    const bool need_u = q < P.max_order && has_eprev;
+                    double r_down = 0.0, r_up = 0.0;
+                    if (need_d || need_u) {
+                        double v[2] = {0.0, 0.0};
+                        const double2* const ecp = ebuf + ecur * DP;
+                        const double2* const epp = ebuf + (ecur ^ 1) * DP;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            if (act[e]) {
+                                const double2 zq = H::row(z, ovf, q, e);
+                                const double2 de = csub(ecp[ii[e]], epp[ii[e]]);
+                                v[0] += cabs2(zq) * w[e] * w[e];
+                                v[1] += cabs2(de) * w[e] * w[e];
+                            }
+                        }
+                        block_sum<NT, 2>(v, red, rphase);
+                        if (need_d) {
+                            const double est_d = sqrt(v[0] / (double)d) / P.tau1[q];
+                            r_down = 1.0 / (1.3 * pow(est_d, 1.0 / q) + 1e-6);
+                        }
+                        if (need_u) {
+                            const double est_u = sqrt(v[1] / (double)d) / P.tau3[q];
+                            r_up = 1.0 / (1.4 * pow(est_u, 1.0 / (q + 2)) + 1e-6);
+                        }
+                    }
+                    double best = r_same;
+                    if (r_down > best) best = r_down;
+                    if (r_up > best) best = r_up;
+                    if (best < 1.1) {
+                        ialth = 3;
+                        ecur ^= 1;  // e_prev = e
+                        has_eprev = true;
+                    } else {
+                        if (best == r_up) {
+                            const double cu = P.l[q][q] / (q + 1);
+                            const double2* const ecp = ebuf + ecur * DP;
+#pragma unroll
+                            for (int e = 0; e < E; ++e)
+                                H::set_row(z, ovf, q + 1, e, act[e] ? cscale(cu, ecp[ii[e]]) : make_double2(0.0, 0.0));
+                            q = q + 1;
+                            STAT(sOrderUp, 1);
+                        } else if (best == r_down) {
+                            q = q - 1;
+                            STAT(sOrderDown, 1);
+                        }
+                        const double m1 = 10.0 < best ? 10.0 : best;
+                        RESCALE(m1 > 0.1 ? m1 : 0.1);
+                    }
+                } else {
+                    ecur ^= 1;  // e_prev = e
+                    has_eprev = true;
+                }
+                // ================= trajectory loop body (trajectory.py:225-246) =======
+                steps_in_segment += 1;
+                if (steps_in_segment > P.max_steps) FAIL(kErrMaxSteps);
+                if (P.nc > 0 && nrm2 < r) {
+                    // locate_jump_time (trajectory.py:157-182)
+                    double v2[2] = {0.0, 0.0};
+                    {
+                        double2 a1[E], a2[E];
+                        HORNER((t_lo - t) / h, a1);
+                        HORNER((t - t) / h, a2);
+#pragma unroll
+                        for (int e = 0; e < E; ++e) if (act[e]) { v2[0] += cabs2(a1[e]); v2[1] += cabs2(a2[e]); }
+                    }
+                    block_sum<NT, 2>(v2, red, rphase);
+                    const double f_lo = v2[0], f_hi = v2[1];
+                    const double tol = 1e-9 * r;
+                    if (f_lo < r - tol || f_hi > r + tol) {
+                        if (tid == 0) R.err_r[row] = r;
+                        FAIL4(kErrBracket, t_lo, t, f_lo, f_hi);
+                    }
+                    double ts;
+                    if (f_lo <= r + tol) {
+                        ts = t_lo;
+                    } else {
+                        double a = t_lo, b = t;
+                        bool found = false;
+                        ts = 0.0;
+                        for (int it = 0; it < 60; ++it) {
+                            const double mid = 0.5 * (a + b);
+                            double v1[1] = {0.0};
+                            {
+                                double2 am[E];
+                                HORNER((mid - t) / h, am);
+#pragma unroll
+                                for (int e = 0; e < E; ++e) if (act[e]) v1[0] += cabs2(am[e]);
+                            }
+                            block_sum<NT, 1>(v1, red, rphase);
+                            STAT(sBisect, 1);
+                            if (fabs(v1[0] - r) <= tol) { ts = mid; found = true; break; }
+                            if (v1[0] > r) a = mid; else b = mid;
+                        }
+                        if (!found) ts = 0.5 * (a + b);
+                    }
+                    if (ts <= P.t_to) {
+                        while (gi < npts && P.times[gi] <= ts) {
+                            double2 pg[E];
+                            HORNER((P.times[gi] - t) / h, pg);
+                            RECORD(pg, gi);
+                            gi++;
+                        }
+                        // psi(t*) and the collapse (trajectory.py:235-241, 133-154)
+                        double2 pst[E];
+                        HORNER((ts - t) / h, pst);
+                        double u;
+                        DRAW(u);
+                        GATHER(pst, xs);
+                        double wts[MAXOPS];
+                        for (int c0 = 0; c0 < P.nc; c0 += KRED) {
+                            double v4[KRED] = {0.0, 0.0, 0.0, 0.0};
+                            for (int kk = 0; kk < KRED; ++kk) {
+                                if (c0 + kk < P.nc) {
+#pragma unroll
+                                    for (int e = 0; e < E; ++e)
+                                        if (act[e]) v4[kk] += cabs2(row_dot(P.c[c0 + kk], ii[e], xs));
+                                }
+                            }
+                            block_sum<NT, KRED>(v4, red, rphase);
+                            for (int kk = 0; kk < KRED; ++kk) if (c0 + kk < P.nc) wts[c0 + kk] = v4[kk];
+                        }
+                        double dp = 0.0;
+                        for (int c = 0; c < P.nc; ++c) dp += wts[c];
+                        if (dp <= 0.0) FAIL(kErrNoSupport);
+                        int idx = 0;
+                        for (int c = 0; c < P.nc; ++c) if (wts[c] > 0.0) idx = c;
+                        double cum = 0.0;
+                        for (int c = 0; c < P.nc; ++c) {
+                            cum += wts[c] / dp;
+                            if (wts[c] > 0.0 && cum >= u) { idx = c; break; }
+                        }
+                        const double scl = 1.0 / sqrt(wts[idx]);
+#pragma unroll
+                        for (int e = 0; e < E; ++e)
+                            pst[e] = act[e] ? cscale(scl, row_dot(P.c[idx], ii[e], xs)) : make_double2(0.0, 0.0);
+                        if (tid == 0 && njumps < R.max_jumps) {
+                            R.jump_t[(size_t)row * R.max_jumps + njumps] = ts;
+                            R.jump_idx[(size_t)row * R.max_jumps + njumps] = idx;
+                        }
+                        njumps++;
+                        STAT(sJumps, 1);
+                        DRAW(r);
+                        COLD_START(ts, pst, h);
+                        steps_in_segment = 0;
+                        continue;
+                    }
+                }
+                while (gi < npts && P.times[gi] <= t) {
+                    double2 pg[E];
+                    HORNER((P.times[gi] - t) / h, pg);
+                    RECORD(pg, gi);
+                    gi++;
+                }
+            }
+        }
+    traj_done:
+        if (tid == 0) {
+            s_stats[sDraws] = (long long)s_stream.n;
+            long long* so = R.stats + (size_t)row * NSTATS;
+#pragma unroll
+            for (int s = 0; s < NSTATS; ++s) so[s] = s_stats[s];
+            R.status[row] = rc;
+            R.jump_count[row] = njumps;
+            if (rc != kOk) atomicMin(R.first_fail, (unsigned long long)row);
+        }
+        __syncthreads();
+    }
+#undef GATHER
+#undef HORNER
+#undef RESCALE
+#undef FAIL
+#undef FAIL4
+#undef DRAW
+#undef RECORD
+#undef COLD_START
+}
+
+#undef STAT
+
+}  // namespace qtm

@@ -1,0 +1,314 @@
+"""Device trajectory engine: the drop-in for the reference's trajectory loop.
+
+``run_gpu(problem, n_total, master_seed)`` has the positional signature and
+the return type of the reference's ``run_inline``
+(/root/reference/pkg/src/mcwf/cluster.py:472-482): it integrates trajectories
+0..n_total-1, averages ⟨E_k⟩(t_j) over them and returns a
+``TrajectoryResult``.  The per-trajectory work (run_single_trajectory,
+trajectory.py:190-250, and the solver it drives, ode.py) runs inside one
+persistent sm_100a kernel per call (csrc/qtm_traj.cuh) behind the C ABI in
+include/qtm.h.
+
+Random streams are per trajectory and keyed by the global index (see
+csrc/qtm_rng.cuh), so the ensemble does not depend on how it is sharded
+over GPUs; the reference's single sequential per-worker stream cannot be
+reproduced in parallel.
+
+``run_sharded`` is the multi-GPU form (one process per GPU): contiguous
+trajectory ranges per rank (partition_trajectories rule, cluster.py:369-377)
+and one all-reduce of the per-point sums.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .packing import PackedProblem, pack_problem
+from .problem import OdeFailure, TrajectoryResult
+
+__all__ = ["DeviceProblem", "RunOutput", "run_gpu", "run_sharded", "partition_trajectories",
+           "raise_for_status", "stats_dict", "flops_model"]
+
+
+def partition_trajectories(n_total: int, n_workers: int) -> list[int]:
+    """Counts per worker: sum n_total, max - min <= 1, remainder to the
+    lowest ranks (cluster.py:369-377)."""
+    if n_total < 1:
+        raise ValueError("n_total must be positive")
+    if n_workers < 1:
+        raise ValueError("n_workers must be positive")
+    base, rem = divmod(n_total, n_workers)
+    return [base + 1 if r < rem else base for r in range(n_workers)]
+
+
+def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    counts = partition_trajectories(n_total, world)
+    begin = sum(counts[:rank])
+    return begin, begin + counts[rank]
+
+
+def _inside(istate: int, detail: str) -> OdeFailure:
+    # run_single_trajectory re-raises solver failures with this suffix
+    # (trajectory.py:247-248)
+    inner = OdeFailure(istate, detail)
+    return OdeFailure(istate, f"{inner} (inside trajectory)")
+
+
+def raise_for_status(code: int, err: dict) -> None:
+    """Raise the reference's exception for a failing trajectory."""
+    t, h = err.get("t", 0.0), err.get("h", 0.0)
+    if code == native.ERR_MAX_STEPS:
+        raise _inside(-1, f"max_steps = {err.get('max_steps')} exhausted in trajectory segment "
+                          f"at t = {t:g}")
+    if code == native.ERR_REPEATED_ERRTEST:
+        raise _inside(-4, f"repeated error-test failures at t = {t:g}")
+    if code == native.ERR_STEP_COLLAPSE:
+        raise _inside(-5, f"step size collapsed to {h:g} at t = {t:g}")
+    if code == native.ERR_CORRECTOR:
+        raise _inside(-5, f"corrector failed to converge at t = {t:g}")
+    if code == native.ERR_BRACKET:
+        f_lo, f_hi, r = err.get("aux", (0.0, 0.0, 0.0))
+        raise RuntimeError(f"jump bracket violated: norm_sq({t:g}) = {f_lo:g}, "
+                           f"norm_sq({h:g}) = {f_hi:g}, r = {r:g}")
+    if code == native.ERR_NO_SUPPORT:
+        raise ValueError("no collapse channel has support on the state")
+    if code == native.ERR_ZERO_VECTOR:
+        raise ValueError("expectation of a zero vector")
+    raise RuntimeError(f"trajectory engine error {code}")
+
+
+def stats_dict(row) -> dict:
+    return {name: int(row[i]) for i, name in enumerate(native.STAT_NAMES)}
+
+
+def flops_model(stats_total: dict, packed: PackedProblem) -> float:
+    """Algorithmic FP64 flops of all step attempts:
+    per attempt m (8 nnz + 15 d) + d (q(q+1) + 4(q+1) + 13)."""
+    d, nnz = packed.dim, packed.g.nnz
+    m = stats_total["corr_iters"]
+    att = stats_total["attempts"]
+    return float(m * (8 * nnz + 15 * d)
+                 + d * (stats_total["sum_qq1"] + 4 * (stats_total["sum_q"] + att) + 13 * att))
+
+
+def bytes_model(stats_total: dict, packed: PackedProblem) -> float:
+    """HBM bytes the state-streaming design would move:
+    16 d (2 (q+1) + 2) per attempt."""
+    d = packed.dim
+    att = stats_total["attempts"]
+    return float(16 * d * (2 * (stats_total["sum_q"] + att) + 2 * att))
+
+
+@dataclass
+class RunOutput:
+    sum: np.ndarray
+    sumsq: np.ndarray
+    values: np.ndarray | None
+    stats: np.ndarray | None
+    stats_total: np.ndarray
+    status: np.ndarray | None
+    jump_count: np.ndarray | None
+    jump_t: np.ndarray | None
+    jump_idx: np.ndarray | None
+    error: dict | None
+    rc: int
+    kernel_ms: float
+    total_ms: float
+    variant: int
+    grid: int
+    launches: int
+    count: int
+
+
+def _p(a, t=C.POINTER(C.c_double)):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+class DeviceProblem:
+    """A problem resident in one GPU's HBM (qtm_problem handle)."""
+
+    def __init__(self, problem, *, device: int = 0, variant: int = -1,
+                 h0_first: float | None = None):
+        self.packed = problem if isinstance(problem, PackedProblem) else \
+            pack_problem(problem, h0_first=h0_first)
+        self.device = device
+        L = native.lib()
+        pk = self.packed
+        keep = []
+
+        def csr(m):
+            keep.extend([m.row_ptr, m.col_ind, m.values])
+            return native.QtmCsr(_p(m.row_ptr, C.POINTER(C.c_int64)),
+                                 _p(m.col_ind, C.POINTER(C.c_int64)), _p(m.values), m.nnz)
+
+        coll = (native.QtmCsr * max(1, pk.n_collapse))(*[csr(c) for c in pk.collapse])
+        expt = (native.QtmCsr * max(1, pk.n_expect))(*[csr(e) for e in pk.expect])
+        desc = native.QtmProblemDesc(
+            native.ABI_VERSION, pk.dim, csr(pk.g), pk.n_collapse, coll, pk.n_expect, expt,
+            _p(pk.psi0), pk.t_from, pk.t_to, pk.n_steps, _p(pk.times), 0, pk.rtol, pk.atol,
+            pk.max_order, pk.max_steps, pk.h0_first, _p(pk.l_table), _p(pk.tau1), _p(pk.tau2),
+            _p(pk.tau3), device, variant)
+        handle = C.c_void_p()
+        rc = L.qtm_problem_create(C.byref(desc), C.byref(handle))
+        if rc != 0:
+            raise RuntimeError(f"qtm_problem_create failed ({rc}): {native.last_error()}")
+        self._handle = handle
+        self._lock = threading.Lock()
+
+    def close(self):
+        if getattr(self, "_handle", None):
+            native.lib().qtm_problem_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def run(self, seed: int, traj_begin: int, traj_end: int, *, stream: str = "philox",
+            script=None, script_fallback: float = 0.999999, max_jumps: int = 0,
+            per_trajectory: bool = True, resident: bool = False,
+            cuda_stream: int | None = None) -> RunOutput:
+        """Integrate global trajectories [traj_begin, traj_end).  With
+        ``per_trajectory`` the per-trajectory series, counters and jump logs
+        come back too; ``resident`` skips those copies entirely."""
+        if self._handle is None:
+            raise RuntimeError("device problem already closed")
+        pk = self.packed
+        n = traj_end - traj_begin
+        n_out = pk.n_expect * pk.n_pts
+        script_arr = script_len = None
+        stride = 0
+        if stream == "scripted":
+            rows = [list(map(float, s)) for s in script]
+            if len(rows) != n:
+                raise ValueError("scripted stream needs one script row per trajectory")
+            stride = max(1, max((len(r) for r in rows), default=1))
+            script_arr = np.zeros((n, stride))
+            script_len = np.zeros(n, np.int64)
+            for i, r in enumerate(rows):
+                script_arr[i, : len(r)] = r
+                script_len[i] = len(r)
+        args = native.QtmRunArgs(int(seed) & 0xFFFFFFFFFFFFFFFF, traj_begin, traj_end,
+                                 native.STREAM_KINDS[stream], _p(script_arr),
+                                 _p(script_len, C.POINTER(C.c_int64)), stride, script_fallback,
+                                 max_jumps, cuda_stream)
+        s = np.zeros(max(n_out, 1))
+        s2 = np.zeros(max(n_out, 1))
+        tot = np.zeros(native.NSTATS, np.int64)
+        want = per_trajectory and not resident
+        vals = np.zeros((n, pk.n_expect, pk.n_pts)) if want else None
+        stats = np.zeros((n, native.NSTATS), np.int64) if want else None
+        status = np.zeros(n, np.int32) if want else None
+        jc = np.zeros(n, np.int64) if want else None
+        jt = np.zeros((n, max_jumps)) if want and max_jumps else None
+        ji = np.zeros((n, max_jumps), np.int32) if want and max_jumps else None
+        out = native.QtmRunOut(_p(s), _p(s2), _p(vals), _p(stats, C.POINTER(C.c_int64)),
+                               _p(tot, C.POINTER(C.c_int64)), _p(status, C.POINTER(C.c_int32)),
+                               _p(jc, C.POINTER(C.c_int64)), _p(jt),
+                               _p(ji, C.POINTER(C.c_int32)))
+        L = native.lib()
+        with self._lock:
+            fn = L.qtm_run_resident if resident else L.qtm_run
+            rc = fn(self._handle, C.byref(args), C.byref(out))
+        err = None
+        if rc != 0:
+            if rc in (native.ERR_ARGS, native.ERR_CUDA, native.ERR_UNSUPPORTED):
+                raise RuntimeError(f"qtm_run failed ({rc}): {native.last_error()}")
+            e = out.error
+            err = {"code": e.code, "traj": e.traj, "t": e.t, "h": e.h, "max_steps": e.max_steps,
+                   "aux": (e.aux0, e.aux1, e.aux2)}
+        return RunOutput(s[:n_out].reshape(pk.n_expect, pk.n_pts),
+                         s2[:n_out].reshape(pk.n_expect, pk.n_pts), vals, stats, tot, status, jc,
+                         jt, ji, err, rc, out.kernel_ms, out.total_ms, out.variant, out.grid,
+                         out.launches, n)
+
+
+def _result(pk: PackedProblem, out: RunOutput, n_total: int, jumps) -> TrajectoryResult:
+    return TrajectoryResult(pk.times, out.sum / n_total, n_total, jumps, sumsq=out.sumsq,
+                            stats=stats_dict(out.stats_total))
+
+
+def _jump_list(out: RunOutput):
+    jumps = []
+    for i in range(out.count):
+        for j in range(int(min(out.jump_count[i], out.jump_t.shape[1]))):
+            jumps.append((float(out.jump_t[i, j]), int(out.jump_idx[i, j])))
+    return jumps
+
+
+def run_gpu(problem, n_total: int, master_seed: int, *, device: int = 0,
+            stream: str = "philox", log_jumps: bool | None = None, max_jumps: int = 1024,
+            variant: int = -1) -> TrajectoryResult:
+    """Drop-in for ``mcwf.run_inline(problem, n_total, master_seed)``:
+    trajectories 0..n_total-1 on one GPU, count-weighted mean over them."""
+    if n_total < 1:
+        raise ValueError("n_total must be positive")
+    with DeviceProblem(problem, device=device, variant=variant) as dp:
+        if log_jumps is None:
+            log_jumps = dp.packed.log_jumps
+        out = dp.run(master_seed, 0, n_total, stream=stream,
+                     max_jumps=max_jumps if log_jumps else 0, per_trajectory=log_jumps)
+        if out.rc != 0:
+            raise_for_status(out.rc, out.error)
+        return _result(dp.packed, out, n_total, _jump_list(out) if log_jumps else None)
+
+
+def run_sharded(problem, n_total: int, master_seed: int, *, rank: int, world_size: int,
+                stream: str = "philox", device: int | None = None, runner=None,
+                group=None) -> TrajectoryResult | None:
+    """One rank of a multi-GPU run (one process per GPU, torch.distributed
+    initialised by the caller).  Rank r integrates its contiguous range of
+    global trajectory indices; the per-point sums, sums of squares, counters
+    and the first failure are combined with one all-reduce.  Returns the
+    TrajectoryResult on every rank.
+
+    ``runner(packed, seed, begin, end, stream) -> RunOutput`` defaults to the
+    device engine on ``device`` (= rank); the CPU multi-process tests inject
+    the oracle here to check the sharding and reduction logic with gloo."""
+    import torch
+    import torch.distributed as dist
+
+    packed = problem if isinstance(problem, PackedProblem) else pack_problem(problem)
+    begin, end = shard_range(n_total, world_size, rank)
+    if runner is None:
+        dev = rank if device is None else device
+        with DeviceProblem(packed, device=dev) as dp:
+            out = dp.run(master_seed, begin, end, stream=stream, per_trajectory=False,
+                         resident=True)
+    else:
+        out = runner(packed, master_seed, begin, end, stream)
+    n_out = packed.n_expect * packed.n_pts
+    fail_row = out.error["traj"] if out.rc != 0 else np.iinfo(np.int64).max
+    backend = dist.get_backend(group)
+    tdev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else \
+        torch.device("cpu")
+    # one float64 all-reduce: [sum | sumsq | stats]
+    buf = torch.from_numpy(np.concatenate([out.sum.ravel(), out.sumsq.ravel(),
+                                           out.stats_total.astype(np.float64)])).to(tdev)
+    dist.all_reduce(buf, group=group)
+    fail = torch.tensor([fail_row], dtype=torch.int64, device=tdev)
+    dist.all_reduce(fail, op=dist.ReduceOp.MIN, group=group)
+    first_fail = int(fail.item())
+    if first_fail != np.iinfo(np.int64).max:
+        if out.rc != 0 and out.error["traj"] == first_fail:
+            raise_for_status(out.rc, out.error)
+        raise RuntimeError(f"trajectory {first_fail} failed on another rank")
+    host = buf.cpu().numpy()
+    s = host[:n_out].reshape(packed.n_expect, packed.n_pts)
+    s2 = host[n_out:2 * n_out].reshape(packed.n_expect, packed.n_pts)
+    stats = host[2 * n_out:].astype(np.int64)
+    return TrajectoryResult(packed.times, s / n_total, n_total, None, sumsq=s2,
+                            stats=stats_dict(stats))

@@ -1,0 +1,191 @@
+"""Device kernels vs the reference (golden fixtures) and vs the C oracle.
+
+Identical per-trajectory streams on both sides: jump counts and channels
+must agree exactly; expectation series, psi-derived values and jump times
+within 1e-6 (BASELINE.json north_star: "same jump sequences and psi(t)
+within 1e-6 ... ensemble <O>(t) within 1e-6 absolute under identical
+streams and within 3 standard errors under independent streams").
+"""
+
+import numpy as np
+import pytest
+
+import goldens
+from paper_1810_03047_b200 import configs, engine, native
+from paper_1810_03047_b200.engine import DeviceProblem, run_gpu
+from paper_1810_03047_b200.packing import pack_problem
+from paper_1810_03047_b200.problem import OdeConfig, OdeFailure, QuantumProblem, RunOptions
+from paper_1810_03047_b200.qops import EffectiveGenerator, OperatorSet, fock, sigma_minus, sigma_z
+from paper_1810_03047_b200.csr import to_csr
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6
+MAXJ = 256
+
+
+def _compare(out, s, i_out, i_s):
+    n = int(s.jump_count[i_s])
+    assert int(out.jump_count[i_out]) == n
+    np.testing.assert_array_equal(out.jump_idx[i_out, :n], s.jump_idx[i_s])
+    np.testing.assert_allclose(out.jump_t[i_out, :n], s.jump_t[i_s], rtol=0, atol=TOL)
+    np.testing.assert_allclose(out.values[i_out], s.values[i_s], rtol=0, atol=TOL)
+
+
+@pytest.mark.parametrize("name", goldens.CONFIG_NAMES)
+@pytest.mark.parametrize("kind", ["philox", "lfsr113"])
+def test_device_matches_reference_goldens(name, kind):
+    g = goldens.load(name)
+    s = g.samples[kind]
+    k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
+    with DeviceProblem(g.problem) as dp:
+        out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ)
+    assert out.rc == 0, out.error
+    assert np.all(out.status == 0)
+    for i in range(k1 - k0):
+        _compare(out, s, i, i)
+    # ensemble over the sample, identical streams
+    np.testing.assert_allclose(out.sum / (k1 - k0), s.values.mean(axis=0), rtol=0, atol=TOL)
+    np.testing.assert_array_equal(out.stats[:, native.STAT_NAMES.index("draws")], s.n_draws)
+
+
+@pytest.mark.parametrize("name", goldens.SCENARIOS)
+def test_device_matches_reference_scenarios(name):
+    g = goldens.load(name)
+    for kind, s in g.samples.items():
+        k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
+        with DeviceProblem(g.problem) as dp:
+            out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ,
+                         script=goldens.SCRIPTS.get(name))
+        assert out.rc == 0, out.error
+        for i in range(k1 - k0):
+            _compare(out, s, i, i)
+
+
+@pytest.mark.parametrize("name,n", [("c1", 500), ("c2", 512), ("c3", 256), ("c4", 256),
+                                    ("c5", 32)])
+def test_device_matches_oracle_identical_streams(name, n, oracle_lib):
+    p = configs.build(name)
+    pk = pack_problem(p)
+    with DeviceProblem(pk) as dp:
+        out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert out.rc == 0, out.error
+    ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert ref["rc"] == 0
+    np.testing.assert_array_equal(out.jump_count, ref["jump_count"])
+    for i in range(n):
+        m = int(ref["jump_count"][i])
+        np.testing.assert_array_equal(out.jump_idx[i, :m], ref["jump_idx"][i, :m])
+        np.testing.assert_allclose(out.jump_t[i, :m], ref["jump_t"][i, :m], rtol=0, atol=TOL)
+    np.testing.assert_allclose(out.values, ref["values"], rtol=0, atol=TOL)
+    np.testing.assert_allclose(out.sum / n, ref["values"].mean(axis=0), rtol=0, atol=TOL)
+
+
+def test_forced_jump_at_ln2():
+    # reference tests/test_trajectory.py:53-67
+    g = goldens.load("decay_forced_jump")
+    with DeviceProblem(g.problem) as dp:
+        out = dp.run(0, 0, 1, stream="scripted", script=goldens.SCRIPTS["decay_forced_jump"],
+                     max_jumps=4)
+    assert out.jump_count[0] == 1 and out.jump_idx[0, 0] == 0
+    t_star = out.jump_t[0, 0]
+    assert abs(t_star - np.log(2.0)) < 1e-6
+    times = g.problem.time_grid()
+    np.testing.assert_allclose(out.values[0, 0, times < t_star], -1.0, atol=1e-9)
+    np.testing.assert_allclose(out.values[0, 0, times > t_star], 1.0, atol=1e-9)
+
+
+def test_closed_rabi_matches_cosine():
+    # reference tests/test_trajectory.py:46-50
+    g = goldens.load("rabi_closed")
+    res = run_gpu(g.problem, 1, 1)
+    omega = 2 * np.pi / 10
+    assert np.abs(res.values[0] - np.cos(2 * omega * res.times)).max() < 10 * 1e-8
+
+
+def test_run_gpu_is_deterministic_and_shard_invariant():
+    p = configs.build("c2")
+    with DeviceProblem(p) as dp:
+        a = dp.run(11, 0, 600, max_jumps=MAXJ)
+        b = dp.run(11, 0, 600, max_jumps=MAXJ)
+        lo = dp.run(11, 0, 250, max_jumps=MAXJ)
+        hi = dp.run(11, 250, 600, max_jumps=MAXJ)
+    np.testing.assert_array_equal(a.values, b.values)
+    np.testing.assert_array_equal(a.sum, b.sum)
+    np.testing.assert_array_equal(a.values[:250], lo.values)
+    np.testing.assert_array_equal(a.values[250:], hi.values)
+
+
+def test_run_gpu_drop_in_signature():
+    p = configs.build("c1", log_jumps=True)
+    res = run_gpu(p, 64, 987654321)
+    assert res.values.shape == (2, 201) and res.n_trajectories == 64
+    assert res.jumps is not None and all(0 <= idx < 1 for _, idx in res.jumps)
+    np.testing.assert_allclose(res.values[:, 0], [1.0, 0.0])
+    se = res.standard_error()
+    assert np.all(np.isfinite(se))
+
+
+def test_max_steps_failure_message():
+    g = goldens.load("c1_max_steps")
+    with pytest.raises(OdeFailure) as exc:
+        run_gpu(g.problem, 4, goldens.SEED)
+    assert str(exc.value) == str(g.raw["max_steps_msg"])
+
+
+def test_no_support_raises_value_error():
+    # norm decays through G but the collapse channel has no support on the
+    # state: reference apply_collapse raises ValueError (trajectory.py:143-144)
+    g = to_csr(-0.5 * np.eye(2, dtype=complex))
+    p = QuantumProblem(generator=EffectiveGenerator(g), collapse_csr=(to_csr(sigma_minus()),),
+                       expect_csr=(to_csr(sigma_z()),), psi0=fock(2, 0), t_from=0.0, t_to=5.0,
+                       n_steps=5, ode=OdeConfig(rtol=1e-8, atol=1e-10))
+    with pytest.raises(ValueError, match="support"):
+        run_gpu(p, 2, 3)
+
+
+@pytest.mark.parametrize("variant", range(5, 11))
+def test_large_variants_agree(variant):
+    # every d<=1024-capable kernel variant (register row budgets 2..10, with
+    # the overflow scratch in use) gives the same trajectories
+    t, e, r = native.variants()[variant]
+    if t * e < 1024:
+        pytest.skip("variant too small for c4")
+    p = configs.build("c4")
+    with DeviceProblem(p, variant=6) as ref, DeviceProblem(p, variant=variant) as dp:
+        a = ref.run(3, 0, 24, max_jumps=MAXJ)
+        b = dp.run(3, 0, 24, max_jumps=MAXJ)
+    np.testing.assert_array_equal(a.jump_count, b.jump_count)
+    np.testing.assert_allclose(a.values, b.values, rtol=0, atol=1e-9)
+
+
+def test_full_size_properties_c4():
+    p = configs.build("c4")
+    with DeviceProblem(p) as dp:
+        out = dp.run(987654321, 0, 4096, per_trajectory=False, resident=True)
+    assert out.rc == 0
+    mean = out.sum / 4096
+    np.testing.assert_array_equal(mean[:, 0], 1.0)  # |up...up>: <sz_i>(0) = +1 exactly
+    assert np.all(np.abs(mean) <= 1.0 + 1e-12)
+    assert np.all(out.sumsq / 4096 <= 1.0 + 1e-12)
+    # mirror symmetry of the open chain: <sz_i> = <sz_{L-1-i}> within 4 SE
+    n = 4096
+    se = np.sqrt(np.maximum(out.sumsq / n - mean ** 2, 0) / n)
+    assert np.all(np.abs(mean - mean[::-1]) <= 4 * np.sqrt(se ** 2 + se[::-1] ** 2) + 1e-12)
+
+
+def test_independent_streams_within_three_sigma(oracle_lib):
+    # GPU ensemble at full N (c2) vs an independent-seed CPU ensemble
+    p = configs.build("c2")
+    pk = pack_problem(p)
+    n_gpu, n_cpu = 5000, 1000
+    with DeviceProblem(pk) as dp:
+        out = dp.run(987654321, 0, n_gpu, per_trajectory=False, resident=True)
+    ref = oracle_lib.run(pk, 12345, 0, n_cpu)
+    mg = out.sum / n_gpu
+    se_g = np.sqrt(np.maximum(out.sumsq / n_gpu - mg ** 2, 0) / n_gpu)
+    mc = ref["values"].mean(axis=0)
+    se_c = ref["values"].std(axis=0, ddof=1) / np.sqrt(n_cpu)
+    z = np.abs(mg - mc) / np.maximum(np.sqrt(se_g ** 2 + se_c ** 2), 1e-12)
+    # 602 points: allow the expected ~0.3 % beyond 3 sigma, none beyond 5
+    assert np.mean(z > 3) < 0.02 and z.max() < 5

@@ -1,0 +1,79 @@
+"""Pin the C oracle (oracle/mcwf_oracle.c) against the reference itself.
+
+The fixtures in tests/golden/ were produced by the reference's own
+``run_single_trajectory`` (see tests/golden/make_golden.py).  Per-trajectory
+streams are identical on both sides, so jump sequences must agree exactly
+and the expectation series / jump times to within 1e-6 (BASELINE.json's
+parity tolerance; in practice the oracle is bit-exact on the small problems
+and within ~1e-7 where the reference's BLAS-ordered dot products differ).
+"""
+
+import numpy as np
+import pytest
+
+import goldens
+from paper_1810_03047_b200.packing import pack_problem
+
+TOL = 1e-6
+
+
+def _check(name, kind, oracle_lib):
+    g = goldens.load(name)
+    s = g.samples[kind]
+    pk = pack_problem(g.problem)
+    k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
+    assert np.array_equal(s.traj, np.arange(k0, k1))
+    r = oracle_lib.run(pk, goldens.SEED, k0, k1, stream=kind, script=goldens.SCRIPTS.get(name))
+    assert r["rc"] == 0, r["error"]
+    np.testing.assert_array_equal(r["jump_count"], s.jump_count)
+    for i in range(len(s.traj)):
+        n = s.jump_count[i]
+        np.testing.assert_array_equal(r["jump_idx"][i, :n], s.jump_idx[i])
+        np.testing.assert_allclose(r["jump_t"][i, :n], s.jump_t[i], rtol=0, atol=TOL)
+    assert np.abs(r["values"] - s.values).max() <= TOL
+    np.testing.assert_array_equal(r["stats"][:, 11], s.n_draws)  # draws consumed
+    return r, s
+
+
+@pytest.mark.parametrize("name", goldens.CONFIG_NAMES)
+@pytest.mark.parametrize("kind", ["philox", "lfsr113"])
+def test_oracle_matches_reference_configs(name, kind, oracle_lib):
+    _check(name, kind, oracle_lib)
+
+
+@pytest.mark.parametrize("name", goldens.SCENARIOS)
+def test_oracle_matches_reference_scenarios(name, oracle_lib):
+    g = goldens.load(name)
+    for kind in g.samples:
+        _check(name, kind, oracle_lib)
+
+
+def test_oracle_bit_exact_on_small_problems(oracle_lib):
+    # d <= 5: no BLAS-ordered reduction differs, the restatement is exact
+    for name in ("c1", "decay_streams", "rabi_collapse", "photon", "unitary"):
+        g = goldens.load(name)
+        for kind, s in g.samples.items():
+            r = oracle_lib.run(pack_problem(g.problem), goldens.SEED, int(s.traj[0]),
+                               int(s.traj[-1]) + 1, stream=kind)
+            np.testing.assert_array_equal(r["values"], s.values)
+
+
+def test_forced_jump_at_ln2(oracle_lib):
+    # reference tests/test_trajectory.py:53-67 with ScriptedDraws [0.5, 0.3, 0.9999999]
+    g = goldens.load("decay_forced_jump")
+    r = oracle_lib.run(pack_problem(g.problem), 0, 0, 1, stream="scripted",
+                       script=goldens.SCRIPTS["decay_forced_jump"])
+    assert r["jump_count"][0] == 1 and r["jump_idx"][0, 0] == 0
+    assert abs(r["jump_t"][0, 0] - np.log(2.0)) < 1e-6
+    times = g.problem.time_grid()
+    v = r["values"][0, 0]
+    np.testing.assert_allclose(v[times < r["jump_t"][0, 0]], -1.0, atol=1e-9)
+    np.testing.assert_allclose(v[times > r["jump_t"][0, 0]], 1.0, atol=1e-9)
+
+
+def test_oracle_threads_do_not_change_results(oracle_lib):
+    g = goldens.load("c2")
+    pk = pack_problem(g.problem)
+    a = oracle_lib.run(pk, 5, 0, 12, n_threads=1)
+    b = oracle_lib.run(pk, 5, 0, 12, n_threads=4)
+    np.testing.assert_array_equal(a["values"], b["values"])
