@@ -122,8 +122,13 @@ typedef struct {
     double aux0, aux1, aux2;        /* bracket: f_lo, f_hi, r */
 } qtm_error;
 
+/* Sums run over the trajectories that completed; a failing trajectory is
+ * excluded and counted in n_failed, and the call returns the failure code of
+ * the lowest failing index (details in `error`), like the reference's first
+ * error.  The caller chooses whether to raise (reference behaviour) or keep
+ * the average over the completed trajectories. */
 typedef struct {
-    double* sum;          /* [n_expect*(n_steps+1)]  sum over trajectories (required) */
+    double* sum;          /* [n_expect*(n_steps+1)]  sum over completed trajectories (required) */
     double* sumsq;        /* [n_expect*(n_steps+1)]  sum of squares (or NULL) */
     double* values;       /* [count][n_expect][n_steps+1] per trajectory (or NULL) */
     int64_t* stats;       /* [count][QTM_NSTATS] (or NULL) */
@@ -138,6 +143,7 @@ typedef struct {
     int32_t variant;      /* kernel variant that ran */
     int32_t grid;         /* CTAs launched */
     int64_t launches;     /* kernels launched by this call */
+    int64_t n_failed;     /* trajectories that failed (excluded from the sums) */
 } qtm_run_out;
 
 int qtm_problem_create(const qtm_problem_desc* desc, qtm_problem** out);

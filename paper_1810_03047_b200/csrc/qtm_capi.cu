@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -26,8 +27,9 @@ namespace qtm {
 // Deterministic ensemble sums: stage 1 sums a fixed chunk of trajectories
 // per (chunk, output) in trajectory order, stage 2 sums the chunk partials
 // in chunk order.  Coalesced over the output index.
-__global__ void ensemble_partial(const double* __restrict__ values, long long n_traj, int n_out,
-                                 int chunk, double* __restrict__ psum, double* __restrict__ psq) {
+__global__ void ensemble_partial(const double* __restrict__ values, const int* __restrict__ status,
+                                 long long n_traj, int n_out, int chunk, double* __restrict__ psum,
+                                 double* __restrict__ psq) {
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     const long long c = blockIdx.y;
     if (o >= n_out) return;
@@ -35,6 +37,7 @@ __global__ void ensemble_partial(const double* __restrict__ values, long long n_
     const long long en = b + chunk < n_traj ? b + chunk : n_traj;
     double s = 0.0, s2 = 0.0;
     for (long long k = b; k < en; ++k) {
+        if (status[k] != 0) continue;  // failed trajectories are excluded from the sums
         const double v = values[k * n_out + o];
         s += v;
         s2 += v * v;
@@ -57,12 +60,16 @@ __global__ void ensemble_final(const double* __restrict__ psum, const double* __
     sumsq[o] = s2;
 }
 
-__global__ void stats_total(const long long* __restrict__ stats, long long n_traj,
-                            long long* __restrict__ total) {
+__global__ void stats_total(const long long* __restrict__ stats, const int* __restrict__ status,
+                            long long n_traj, long long* __restrict__ total) {
     const int s = threadIdx.x;
-    if (s >= NSTATS) return;
+    if (s > NSTATS) return;
     long long acc = 0;
-    for (long long k = 0; k < n_traj; ++k) acc += stats[k * NSTATS + s];
+    if (s == NSTATS) {  // slot NSTATS: number of failed trajectories
+        for (long long k = 0; k < n_traj; ++k) acc += status[k] != 0;
+    } else {
+        for (long long k = 0; k < n_traj; ++k) acc += stats[k * NSTATS + s];
+    }
     total[s] = acc;
 }
 
@@ -119,21 +126,38 @@ int auto_variant(int64_t d) {
     return best;
 }
 
+// Device memory comes from the device's default stream-ordered pool with an
+// unlimited release threshold: freeing a problem returns its blocks to the
+// pool without synchronising the device or unmapping, and the next problem
+// reuses them.
+void ensure_pool(int device) {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t threshold = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    done[device] = true;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
-    cudaError_t ensure(size_t count) {
+    cudaError_t ensure(size_t count, cudaStream_t s) {
         if (count <= n && p) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
-        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), s);
         if (e == cudaSuccess) n = std::max<size_t>(count, 1);
         return e;
     }
-    void release() {
-        if (p) cudaFree(p);
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }
@@ -144,6 +168,7 @@ struct DevBuf {
 struct qtm_problem {
     int device = 0;
     int variant = -1;
+    size_t smem = 0;  // dynamic shared memory of a launch (fixed part + staged operator)
     int64_t dim = 0, nnz_total = 0;
     int n_expect = 0, n_collapse = 0;
     int64_t n_pts = 0;
@@ -161,6 +186,15 @@ struct qtm_problem {
 };
 
 namespace {
+
+template <typename T>
+cudaError_t upload(qtm_problem* p, T** dst, const void* src, size_t count) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(dst), std::max<size_t>(count, 1) * sizeof(T), p->stream);
+    if (e != cudaSuccess) return e;
+    p->allocs.push_back(*dst);
+    if (count && src) e = cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, p->stream);
+    return e;
+}
 
 int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const char* what) {
     if (!m.row_ptr || (m.nnz > 0 && (!m.col_ind || !m.values)))
@@ -182,15 +216,9 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
     int* drp = nullptr;
     int* dci = nullptr;
     double2* dv = nullptr;
-    CUDA_TRY(cudaMalloc(&drp, sizeof(int) * (n + 1)));
-    p->allocs.push_back(drp);
-    CUDA_TRY(cudaMalloc(&dci, sizeof(int) * ci.size()));
-    p->allocs.push_back(dci);
-    CUDA_TRY(cudaMalloc(&dv, sizeof(double2) * std::max<int64_t>(m.nnz, 1)));
-    p->allocs.push_back(dv);
-    CUDA_TRY(cudaMemcpy(drp, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(dci, ci.data(), sizeof(int) * ci.size(), cudaMemcpyHostToDevice));
-    if (m.nnz) CUDA_TRY(cudaMemcpy(dv, m.values, sizeof(double2) * m.nnz, cudaMemcpyHostToDevice));
+    CUDA_TRY(upload(p, &drp, rp.data(), n + 1));
+    CUDA_TRY(upload(p, &dci, ci.data(), ci.size()));
+    CUDA_TRY(upload(p, &dv, m.values, (size_t)m.nnz));
     out->rp = drp;
     out->ci = dci;
     out->v = dv;
@@ -198,16 +226,101 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
     return QTM_OK;
 }
 
+// Sliced-ELL copy of G for shared-memory staging (see DevProblem::sell_*).
+// Returns false (and leaves sell_mode = 0) when the operator cannot be
+// encoded (dimension > 65536 or > 65533 distinct off-diagonal values) or the
+// staged copy does not fit next to the kernel's fixed shared memory.
+int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
+               size_t smem_cap, bool* staged) {
+    *staged = false;
+    const int dp = nt * ncomp;
+    const int nslices = dp / 32, nw = nt / 32;
+    if (n > 65536) return QTM_OK;
+    std::vector<int> width(nslices, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int len = (int)(g.row_ptr[i + 1] - g.row_ptr[i]);
+        width[i / 32] = std::max(width[i / 32], len);
+    }
+    // uniform width per warp: warp w walks slices w + nw*e together
+    for (int w = 0; w < nw; ++w) {
+        int m = 0;
+        for (int e = 0; e < ncomp; ++e) m = std::max(m, width[w + nw * e]);
+        for (int e = 0; e < ncomp; ++e) width[w + nw * e] = m;
+    }
+    std::vector<int> off(nslices, 0);
+    int total = 0;
+    for (int sl = 0; sl < nslices; ++sl) {
+        off[sl] = total;
+        total += width[sl] * 32;
+    }
+    std::vector<double2> dict(1, make_double2(0.0, 0.0));
+    std::vector<double2> diag(dp, make_double2(0.0, 0.0));
+    std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: col 0, value index 0 (= 0.0)
+    struct Key {
+        uint64_t a, b;
+        bool operator<(const Key& o) const { return a < o.a || (a == o.a && b < o.b); }
+    };
+    std::map<Key, int> index;
+    for (int64_t i = 0; i < n; ++i) {
+        const int sl = (int)(i / 32), lane = (int)(i % 32);
+        int k = 0;
+        for (int64_t j = g.row_ptr[i]; j < g.row_ptr[i + 1]; ++j, ++k) {
+            const double re = g.values[2 * j], im = g.values[2 * j + 1];
+            uint32_t vi;
+            if (g.col_ind[j] == i) {
+                diag[i] = make_double2(re, im);
+                vi = 0xFFFFu;
+            } else {
+                Key key;
+                memcpy(&key.a, &re, 8);
+                memcpy(&key.b, &im, 8);
+                auto it = index.find(key);
+                if (it == index.end()) {
+                    if (dict.size() >= 0xFFFEu) return QTM_OK;  // too many distinct values
+                    it = index.emplace(key, (int)dict.size()).first;
+                    dict.push_back(make_double2(re, im));
+                }
+                vi = (uint32_t)it->second;
+            }
+            ent[off[sl] + k * 32 + lane] = (uint32_t)g.col_ind[j] | (vi << 16);
+        }
+    }
+    const size_t bytes = sizeof(double2) * (dict.size() + dp) + sizeof(uint32_t) * ent.size();
+    if (fixed_smem + bytes > smem_cap) return QTM_OK;
+    uint32_t* d_ent = nullptr;
+    double2 *d_dict = nullptr, *d_diag = nullptr;
+    int *d_off = nullptr, *d_w = nullptr;
+    CUDA_TRY(upload(p, &d_ent, ent.data(), ent.size()));
+    CUDA_TRY(upload(p, &d_dict, dict.data(), dict.size()));
+    CUDA_TRY(upload(p, &d_diag, diag.data(), (size_t)dp));
+    CUDA_TRY(upload(p, &d_off, off.data(), (size_t)nslices));
+    CUDA_TRY(upload(p, &d_w, width.data(), (size_t)nslices));
+    DevProblem& P = p->dp;
+    P.sell_mode = 1;
+    P.sell_entries = (int)ent.size();
+    P.sell_dict_n = (int)dict.size();
+    P.sell_ent = d_ent;
+    P.sell_dict = d_dict;
+    P.sell_off = d_off;
+    P.sell_w = d_w;
+    P.diag = d_diag;
+    p->smem = fixed_smem + bytes;
+    *staged = true;
+    return QTM_OK;
+}
+
 void free_problem(qtm_problem* p) {
     if (!p) return;
     cudaSetDevice(p->device);
-    for (void* a : p->allocs) cudaFree(a);
-    p->values.release(); p->err.release(); p->err_r.release(); p->psum.release(); p->psq.release();
-    p->sum.release(); p->sumsq.release(); p->jump_t.release(); p->script.release();
-    p->stats.release(); p->jump_count.release(); p->script_len.release(); p->stats_tot.release();
-    p->status.release(); p->jump_idx.release(); p->zovf.release(); p->ctl.release();
+    cudaStream_t s = p->stream;
+    for (void* a : p->allocs) cudaFreeAsync(a, s);
+    p->values.release(s); p->err.release(s); p->err_r.release(s); p->psum.release(s); p->psq.release(s);
+    p->sum.release(s); p->sumsq.release(s); p->jump_t.release(s); p->script.release(s);
+    p->stats.release(s); p->jump_count.release(s); p->script_len.release(s); p->stats_tot.release(s);
+    p->status.release(s); p->jump_idx.release(s); p->zovf.release(s); p->ctl.release(s);
+    if (s) cudaStreamSynchronize(s);
     for (auto& e : p->ev) if (e) cudaEventDestroy(e);
-    if (p->stream) cudaStreamDestroy(p->stream);
+    if (s) cudaStreamDestroy(s);
     delete p;
 }
 
@@ -265,6 +378,11 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         delete p;
         return set_error(QTM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
     }
+    ensure_pool(d->device);
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete p;
+        return set_error(QTM_ERR_CUDA, "cudaStreamCreate failed");
+    }
     int rc = QTM_OK;
     DevProblem& P = p->dp;
     P.d = (int)d->dim;
@@ -283,6 +401,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         P.tau1[q] = d->tau1[q];
         P.tau2[q] = d->tau2[q];
         P.tau3[q] = d->tau3[q];
+        P.conit[q] = 0.5 / (q + 2);
+        P.rq1[q] = 1.0 / (q + 1);
+        P.rq0[q] = q ? 1.0 / q : 0.0;
+        P.rq2[q] = 1.0 / (q + 2);
     }
     rc = upload_csr(p, d->generator, d->dim, &P.g, "generator");
     for (int c = 0; rc == QTM_OK && c < d->n_collapse; ++c) rc = upload_csr(p, d->collapse[c], d->dim, &P.c[c], "collapse");
@@ -290,26 +412,32 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (rc == QTM_OK) {
         double2* psi0 = nullptr;
         double* times = nullptr;
-        if (cudaMalloc(&psi0, sizeof(double2) * d->dim) != cudaSuccess ||
-            cudaMalloc(&times, sizeof(double) * p->n_pts) != cudaSuccess) {
-            rc = set_error(QTM_ERR_CUDA, "cudaMalloc psi0/times failed");
+        if (upload(p, &psi0, d->psi0, (size_t)d->dim) != cudaSuccess ||
+            upload(p, &times, d->times, (size_t)p->n_pts) != cudaSuccess) {
+            rc = set_error(QTM_ERR_CUDA, "device allocation of psi0/times failed");
         } else {
-            p->allocs.push_back(psi0);
-            p->allocs.push_back(times);
-            cudaMemcpy(psi0, d->psi0, sizeof(double2) * d->dim, cudaMemcpyHostToDevice);
-            cudaMemcpy(times, d->times, sizeof(double) * p->n_pts, cudaMemcpyHostToDevice);
             P.psi0 = psi0;
             P.times = times;
         }
     }
-    if (rc == QTM_OK && cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
-        rc = set_error(QTM_ERR_CUDA, "cudaStreamCreate failed");
     for (int i = 0; rc == QTM_OK && i < 4; ++i)
         if (cudaEventCreate(&p->ev[i]) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "cudaEventCreate failed");
-    if (rc == QTM_OK && var.smem > 48 * 1024 &&
-        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)var.smem) != cudaSuccess)
+    int smem_cap = 0;
+    if (rc == QTM_OK && cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device) != cudaSuccess)
+        rc = set_error(QTM_ERR_CUDA, "cudaDeviceGetAttribute(smem opt-in) failed");
+    p->smem = var.smem;
+    if (rc == QTM_OK) {
+        bool staged = false;
+        // static __shared__ of the kernel (row, counters, stream) stays below 1 KB
+        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem,
+                        (size_t)smem_cap - 1024, &staged);
+    }
+    if (rc == QTM_OK && p->smem > 48 * 1024 &&
+        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap - 1024) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
-    if (rc == QTM_OK && p->ctl.ensure(2) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "cudaMalloc ctl failed");
+    if (rc == QTM_OK && p->ctl.ensure(2, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
+    if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)
+        rc = set_error(QTM_ERR_CUDA, "problem upload failed");
     if (rc != QTM_OK) {
         free_problem(p);
         return rc;
@@ -333,6 +461,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     const int n_out = p->n_expect * (int)p->n_pts;
     memset(&o->error, 0, sizeof(o->error));
     o->kernel_ms = o->total_ms = 0.f;
+    o->n_failed = 0;
     o->variant = p->variant;
     o->launches = 0;
     cudaStream_t s = a->cuda_stream ? (cudaStream_t)a->cuda_stream : p->stream;
@@ -346,31 +475,31 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     const Variant& var = variants()[p->variant];
     int dev_sms = 0, per_sm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, var.smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
     if (per_sm < 1) return set_error(QTM_ERR_CUDA, "kernel variant cannot be resident (registers/smem)");
     const long long grid = std::min<long long>((long long)dev_sms * per_sm, count);
     o->grid = (int32_t)grid;
 
-    CUDA_TRY(p->values.ensure((size_t)count * std::max(n_out, 1)));
-    CUDA_TRY(p->stats.ensure((size_t)count * QTM_NSTATS));
-    CUDA_TRY(p->status.ensure(count));
-    CUDA_TRY(p->err.ensure((size_t)count * 4));
-    CUDA_TRY(p->err_r.ensure(count));
-    CUDA_TRY(p->jump_count.ensure(count));
-    CUDA_TRY(p->jump_t.ensure((size_t)count * std::max<long long>(max_jumps, 1)));
-    CUDA_TRY(p->jump_idx.ensure((size_t)count * std::max<long long>(max_jumps, 1)));
-    CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS));
+    CUDA_TRY(p->values.ensure((size_t)count * std::max(n_out, 1), s));
+    CUDA_TRY(p->stats.ensure((size_t)count * QTM_NSTATS, s));
+    CUDA_TRY(p->status.ensure(count, s));
+    CUDA_TRY(p->err.ensure((size_t)count * 4, s));
+    CUDA_TRY(p->err_r.ensure(count, s));
+    CUDA_TRY(p->jump_count.ensure(count, s));
+    CUDA_TRY(p->jump_t.ensure((size_t)count * std::max<long long>(max_jumps, 1), s));
+    CUDA_TRY(p->jump_idx.ensure((size_t)count * std::max<long long>(max_jumps, 1), s));
+    CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS + 1, s));
     const int DP = var.threads * var.comps;
-    if (var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP));
+    if (var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
     const int chunk = 256;
     const int n_chunks = (int)((count + chunk - 1) / chunk);
-    CUDA_TRY(p->psum.ensure((size_t)n_chunks * std::max(n_out, 1)));
-    CUDA_TRY(p->psq.ensure((size_t)n_chunks * std::max(n_out, 1)));
-    CUDA_TRY(p->sum.ensure(std::max(n_out, 1)));
-    CUDA_TRY(p->sumsq.ensure(std::max(n_out, 1)));
+    CUDA_TRY(p->psum.ensure((size_t)n_chunks * std::max(n_out, 1), s));
+    CUDA_TRY(p->psq.ensure((size_t)n_chunks * std::max(n_out, 1), s));
+    CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));
+    CUDA_TRY(p->sumsq.ensure(std::max(n_out, 1), s));
     if (a->stream_kind == QTM_STREAM_SCRIPTED) {
-        CUDA_TRY(p->script.ensure((size_t)count * std::max<int64_t>(a->script_stride, 1)));
-        CUDA_TRY(p->script_len.ensure(count));
+        CUDA_TRY(p->script.ensure((size_t)count * std::max<int64_t>(a->script_stride, 1), s));
+        CUDA_TRY(p->script_len.ensure(count, s));
         CUDA_TRY(cudaMemcpyAsync(p->script.p, a->script, sizeof(double) * count * a->script_stride,
                                  cudaMemcpyHostToDevice, s));
         CUDA_TRY(cudaMemcpyAsync(p->script_len.p, a->script_len, sizeof(int64_t) * count,
@@ -403,18 +532,18 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     R.first_fail = p->ctl.p + 1;
     void* kargs[] = {(void*)&p->dp, (void*)&R};
     CUDA_TRY(cudaEventRecord(p->ev[1], s));
-    CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)grid), dim3(var.threads), kargs, var.smem, s));
+    CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)grid), dim3(var.threads), kargs, p->smem, s));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev[2], s));
     int64_t launches = 1;
     if (n_out > 0) {
         dim3 g1((n_out + 127) / 128, n_chunks);
-        ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, count, n_out, chunk, p->psum.p, p->psq.p);
+        ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, p->status.p, count, n_out, chunk, p->psum.p, p->psq.p);
         ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, n_chunks, n_out, p->sum.p,
                                                            p->sumsq.p);
         launches += 2;
     }
-    stats_total<<<1, 32, 0, s>>>(p->stats.p, count, p->stats_tot.p);
+    stats_total<<<1, 32, 0, s>>>(p->stats.p, p->status.p, count, p->stats_tot.p);
     launches += 1;
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev[3], s));
@@ -424,8 +553,8 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     }
     unsigned long long ctl_out[2];
     CUDA_TRY(cudaMemcpyAsync(ctl_out, p->ctl.p, sizeof(ctl_out), cudaMemcpyDeviceToHost, s));
-    if (o->stats_total)
-        CUDA_TRY(cudaMemcpyAsync(o->stats_total, p->stats_tot.p, sizeof(int64_t) * QTM_NSTATS, cudaMemcpyDeviceToHost, s));
+    long long tot_host[QTM_NSTATS + 1];
+    CUDA_TRY(cudaMemcpyAsync(tot_host, p->stats_tot.p, sizeof(tot_host), cudaMemcpyDeviceToHost, s));
     if (copy_per_traj) {
         if (o->values && n_out > 0)
             CUDA_TRY(cudaMemcpyAsync(o->values, p->values.p, sizeof(double) * count * n_out, cudaMemcpyDeviceToHost, s));
@@ -444,6 +573,8 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     cudaEventElapsedTime(&o->kernel_ms, p->ev[1], p->ev[2]);
     cudaEventElapsedTime(&o->total_ms, p->ev[0], p->ev[3]);
     o->launches = launches;
+    if (o->stats_total) memcpy(o->stats_total, tot_host, sizeof(int64_t) * QTM_NSTATS);
+    o->n_failed = tot_host[QTM_NSTATS];
     if (ctl_out[1] != ~0ull) {
         const long long row = (long long)ctl_out[1];
         int32_t code = 0;

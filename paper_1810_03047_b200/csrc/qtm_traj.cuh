@@ -67,8 +67,24 @@ struct DevProblem {
     DevCsr e[MAXOPS];
     const double2* psi0;
     const double* times;
+    // G in sliced-ELL form for shared-memory staging (built per kernel
+    // variant on the host): slice = 32 consecutive rows, entries stored
+    // [slice][k][lane] as uint32 (col | value-index << 16), widths padded to
+    // be uniform per warp; value index 0xFFFF = the row's diagonal (kept in a
+    // register), other indices point into a dictionary of distinct values
+    // (index 0 = 0.0, used for padding).  sell_mode 0 = plain CSR via L1/L2.
+    int sell_mode;
+    int sell_entries, sell_dict_n;
+    const uint32_t* sell_ent;
+    const double2* sell_dict;
+    const int* sell_off;    // [DP/32] first entry of each slice
+    const int* sell_w;      // [DP/32] width of each slice
+    const double2* diag;    // [DP] diagonal of G (0 where absent)
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
+    // per-order constants the reference evaluates inline, tabulated on the
+    // host with the same IEEE operations: 0.5/(q+2), 1/(q+1), 1/q, 1/(q+2)
+    double conit[LROWS], rq1[LROWS], rq0[LROWS], rq2[LROWS];
 };
 
 struct RunParams {
@@ -115,6 +131,35 @@ __device__ __forceinline__ double2 row_dot(const DevCsr& m, int i, const double2
     return make_double2(sr, si);
 }
 
+// f = G x for this thread's E rows from the staged sliced-ELL copy: the E
+// rows' chains are interleaved for ILP; each row is still summed in column
+// order (entries k ascending), so the rounding matches row_dot exactly.
+template <int NT, int E>
+__device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
+                                          const double2* __restrict__ dict,
+                                          const double2* __restrict__ diag, const int (&off)[E],
+                                          int width, const double2* __restrict__ x,
+                                          double2 (&out)[E]) {
+    const int lane = threadIdx.x & 31;
+    double sr[E], si[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
+#pragma unroll 4
+    for (int k = 0; k < width; ++k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const uint32_t u = ent[off[e] + k * 32 + lane];
+            const unsigned vi = u >> 16;
+            const double2 v = vi == 0xFFFFu ? diag[threadIdx.x + NT * e] : dict[vi];
+            const double2 xv = x[u & 0xFFFFu];
+            sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
+            si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] = make_double2(sr[e], si[e]);
+}
+
 // Bitwise-identical sums on every thread of the CTA: xor-butterfly inside
 // each warp (a+b == b+a at every level, so all lanes agree), lane 0 of every
 // warp publishes its partial, then every warp loads the NW partials one per
@@ -158,9 +203,79 @@ struct Hist {
     using Z = double2[RREG][E];
     using O = double2* [E];
 
+    // ---- order-specialised register paths (q + 1 <= RREG): straight-line
+    // code, no per-row guards.  Dispatch by switch on the uniform order.
+    template <int Q>
+    __device__ __forceinline__ static void predict_q(Z& z) {
+#pragma unroll
+        for (int r = 0; r < Q; ++r)
+#pragma unroll
+            for (int j = Q - 1; j >= r; --j)
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[j][e] = cadd(z[j][e], z[j + 1][e]);
+    }
+    template <int Q>
+    __device__ __forceinline__ static void undo_q(Z& z) {
+#pragma unroll
+        for (int r = Q - 1; r >= 0; --r)
+#pragma unroll
+            for (int j = r; j < Q; ++j)
+#pragma unroll
+                for (int e = 0; e < E; ++e) z[j][e] = csub(z[j][e], z[j + 1][e]);
+    }
+    template <int Q>
+    __device__ __forceinline__ static void rescale_q(Z& z, double ratio) {
+        double f = 1.0;
+#pragma unroll
+        for (int j = 1; j <= Q; ++j) {
+            f *= ratio;
+#pragma unroll
+            for (int e = 0; e < E; ++e) z[j][e] = cscale(f, z[j][e]);
+        }
+    }
+    template <int Q>
+    __device__ __forceinline__ static void commit_q(Z& z, const double* l, const double2 (&ev)[E]) {
+#pragma unroll
+        for (int j = 0; j <= Q; ++j) {
+            const double lj = l[j];
+#pragma unroll
+            for (int e = 0; e < E; ++e) z[j][e] = cadd(z[j][e], cscale(lj, ev[e]));
+        }
+    }
+    template <int Q>
+    __device__ __forceinline__ static void horner_q(const Z& z, double s, double2 (&out)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = z[Q][e];
+#pragma unroll
+        for (int j = Q - 1; j >= 0; --j)
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[e] = cadd(cscale(s, out[e]), z[j][e]);
+    }
+
+#define QTM_QSWITCH(CALL)                                                    \
+    switch (q) {                                                             \
+        case 1: if constexpr (2 <= RREG) { CALL(1); return; } break;         \
+        case 2: if constexpr (3 <= RREG) { CALL(2); return; } break;         \
+        case 3: if constexpr (4 <= RREG) { CALL(3); return; } break;         \
+        case 4: if constexpr (5 <= RREG) { CALL(4); return; } break;         \
+        case 5: if constexpr (6 <= RREG) { CALL(5); return; } break;         \
+        case 6: if constexpr (7 <= RREG) { CALL(6); return; } break;         \
+        case 7: if constexpr (8 <= RREG) { CALL(7); return; } break;         \
+        case 8: if constexpr (9 <= RREG) { CALL(8); return; } break;         \
+        case 9: if constexpr (10 <= RREG) { CALL(9); return; } break;        \
+        case 10: if constexpr (11 <= RREG) { CALL(10); return; } break;      \
+        case 11: if constexpr (12 <= RREG) { CALL(11); return; } break;      \
+        case 12: if constexpr (13 <= RREG) { CALL(12); return; } break;      \
+        default: break;                                                      \
+    }
+
+    // ---- general paths (any q; rows >= RREG in the overflow column)
     // zp = Pascal(z) in place, passes r = 0..q-1, j = q-1 down to r
     // (_kernels.py:133-137)
     __device__ __forceinline__ static void predict(Z& z, O& ovf, int q) {
+#define CALL_(Q) predict_q<Q>(z)
+        QTM_QSWITCH(CALL_)
+#undef CALL_
         for (int r = 0; r < q; ++r) {
             for (int j = q - 1; j >= (r > RREG ? r : RREG); --j) {
 #pragma unroll
@@ -183,6 +298,9 @@ struct Hist {
 
     // inverse of predict (rejected attempt): passes r = q-1..0, j = r..q-1
     __device__ __forceinline__ static void undo(Z& z, O& ovf, int q) {
+#define CALL_(Q) undo_q<Q>(z)
+        QTM_QSWITCH(CALL_)
+#undef CALL_
         for (int r = q - 1; r >= 0; --r) {
 #pragma unroll
             for (int j = 0; j < RREG - 1; ++j) {
@@ -206,6 +324,9 @@ struct Hist {
     // z[j] *= ratio^j, j = 1..q, ratio^j by repeated multiplication
     // (nordsieck_rescale, _kernels.py:107-114)
     __device__ __forceinline__ static void rescale(Z& z, O& ovf, int q, double ratio) {
+#define CALL_(Q) rescale_q<Q>(z, ratio)
+        QTM_QSWITCH(CALL_)
+#undef CALL_
         double f = 1.0;
 #pragma unroll
         for (int j = 1; j < RREG; ++j) {
@@ -225,6 +346,9 @@ struct Hist {
     // z[j] += l_j e, j = 0..q (_kernels.py:187-191)
     __device__ __forceinline__ static void commit(Z& z, O& ovf, int q, const double* l,
                                                   const double2 (&ev)[E]) {
+#define CALL_(Q) commit_q<Q>(z, l, ev)
+        QTM_QSWITCH(CALL_)
+#undef CALL_
 #pragma unroll
         for (int j = 0; j < RREG; ++j) {
             if (j <= q) {
@@ -256,6 +380,9 @@ struct Hist {
 
     // psi(s) = Horner over rows q..0 (nordsieck_eval, _kernels.py:61-69)
     __device__ __forceinline__ static void horner(const Z& z, O& ovf, int q, double s, double2 (&out)[E]) {
+#define CALL_(Q) horner_q<Q>(z, s, out)
+        QTM_QSWITCH(CALL_)
+#undef CALL_
 #pragma unroll
         for (int e = 0; e < E; ++e) out[e] = row(z, ovf, q, e);
         for (int j = q - 1; j >= RREG; --j) {
@@ -270,6 +397,7 @@ struct Hist {
             }
         }
     }
+#undef QTM_QSWITCH
 };
 
 // ------------------------------------------------------------- the kernel
@@ -278,7 +406,8 @@ struct TrajKernel {
     static constexpr int DP = NT * E;  // padded state length
     static constexpr int NW = NT / 32;
 
-    static constexpr size_t smem_bytes() {
+    // fixed part of the dynamic shared memory; the staged operator follows
+    __host__ __device__ static constexpr size_t smem_bytes() {
         return sizeof(double2) * (size_t)DP * 4 + sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1);
     }
 };
@@ -318,6 +447,33 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     for (int e = 0; e < E; ++e)
         ovf[e] = (RREG < LROWS) ? R.zovf + (size_t)blockIdx.x * (LROWS - RREG) * DP + ii[e] : nullptr;
 
+    // ---- stage G (sliced ELL + value dictionary) in shared memory once
+    double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
+                                                       TrajKernel<NT, E, RREG>::smem_bytes());
+    double2* const s_diag = s_dict + P.sell_dict_n;
+    uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_diag + DP);
+    int goff[E], gwidth = 0;
+    if (P.sell_mode) {
+        for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
+        for (int i = tid; i < DP; i += NT) s_diag[i] = P.diag[i];
+        for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
+        const int warp = tid >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) goff[e] = P.sell_off[warp + (NT / 32) * e];
+        gwidth = P.sell_w[warp];
+        __syncthreads();
+    }
+// f[E] = G x (x gathered in shared memory)
+#define GSPMV(xs, f)                                                         \
+    do {                                                                     \
+        if (P.sell_mode) {                                                   \
+            sell_spmv<NT, E>(s_ent, s_dict, s_diag, goff, gwidth, (xs), f);  \
+        } else {                                                             \
+            _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
+                f[e] = act[e] ? row_dot(P.g, ii[e], (xs)) : make_double2(0.0, 0.0); \
+        }                                                                    \
+    } while (0)
+
     int gbuf = 0, rphase = 0, ecur = 0;
 
     for (;;) {
@@ -334,6 +490,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 
         long long njumps = 0;
         int rc = kOk;
+        // hot per-attempt counters live in registers (folded into s_stats at
+        // the end of the trajectory); rare events go straight to s_stats
+        unsigned c_att = 0, c_q = 0, c_qq = 0, c_it = 0, c_steps = 0;
 
         double2 z[RREG][E];  // Nordsieck history rows 0..RREG-1 (registers)
         double w[E];         // error weights 1/(atol + rtol |z0_i|)
@@ -414,10 +573,11 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         t = (t0_); t_lo = t; q = 1; h = (h0_);                               \
         GATHER(y0, xs__);                                                    \
         STAT(sNfe, 1);                                                       \
+        double2 f__[E];                                                      \
+        GSPMV(xs__, f__);                                                    \
         _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
-            const double2 f__ = act[e] ? row_dot(P.g, ii[e], xs__) : make_double2(0.0, 0.0); \
             z[0][e] = (y0)[e];                                               \
-            z[1][e] = cscale(h, f__);                                        \
+            z[1][e] = cscale(h, f__[e]);                                     \
             _Pragma("unroll") for (int j = 2; j < RREG; ++j) z[j][e] = make_double2(0.0, 0.0); \
             w[e] = act[e] ? 1.0 / (P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
         }                                                                    \
@@ -443,9 +603,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 double est = 0.0, nrm2 = 0.0;
                 for (;;) {
                     if (t + h == t) FAIL(kErrStepCollapse);
-                    STAT(sAttempts, 1);
-                    STAT(sSumQ, q);
-                    STAT(sSumQQ1, q * (q + 1));
+                    c_att++;
+                    c_q += q;
+                    c_qq += q * (q + 1);
                     if (q + 1 > RREG) STAT(sOverflow, 1);
                     // predict: in-place Pascal triangle (_kernels.py:133-137)
                     H::predict(z, ovf, q);
@@ -454,7 +614,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     // and writes its update into gath[gbuf^1], which the
                     // reduction barrier then publishes for iteration m+1.
                     const double l0 = P.l[q][0];
-                    const double conit = 0.5 / (q + 2);
+                    const double conit = P.conit[q];
                     bool converged = false;
                     double delp = 0.0, del = 0.0, acc_e = 0.0;
                     {
@@ -467,13 +627,14 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     for (int m = 0; m < 3; ++m) {
                         const double2* const cur = gath + gbuf * DP;
                         double2* const nxt = gath + (gbuf ^ 1) * DP;
-                        STAT(sNfe, 1);
-                        STAT(sCorrIters, 1);
+                        c_it++;
                         double v[3] = {0.0, 0.0, 0.0};
+                        double2 fg[E];
+                        GSPMV(cur, fg);
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
                             if (act[e]) {
-                                const double2 f = row_dot(P.g, ii[e], cur);
+                                const double2 f = fg[e];
                                 const double2 z1 = z[1][e], z0 = z[0][e];
                                 const double2 ei = csub(cscale(h, f), z1);
                                 const double2 yn = cadd(z0, cscale(l0, ei));
@@ -530,15 +691,14 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         for (int e = 0; e < E; ++e) y0c[e] = z[0][e];
                         GATHER(y0c, xs);
                         STAT(sNfe, 1);
+                        double2 fr[E];
+                        GSPMV(xs, fr);
 #pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            const double2 f = act[e] ? row_dot(P.g, ii[e], xs) : make_double2(0.0, 0.0);
-                            z[1][e] = cscale(h, f);
-                        }
+                        for (int e = 0; e < E; ++e) z[1][e] = cscale(h, fr[e]);
                         has_eprev = false;
                         ialth = q + 1;
                     } else {
-                        const double rr = 1.0 / (1.2 * pow(est, 1.0 / (q + 1)) + 1e-6);
+                        const double rr = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
                         const double m1 = 0.9 < rr ? 0.9 : rr;
                         RESCALE(m1 > 0.1 ? m1 : 0.1);
                     }
@@ -546,7 +706,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 // accepted step bookkeeping (ode.py:281-292)
                 t_lo = t;
                 t += h;
-                STAT(sSteps, 1);
+                c_steps++;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = z[0][e];
@@ -555,7 +715,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 ialth -= 1;
                 if (ialth == 0) {
                     // _order_step_control (ode.py:441-466)
-                    const double r_same = 1.0 / (1.2 * pow(est, 1.0 / (q + 1)) + 1e-6);
+                    const double r_same = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
                     const bool need_d = q > 1;
                     const bool need_u = q < P.max_order && has_eprev;
                     double r_down = 0.0, r_up = 0.0;
@@ -575,11 +735,11 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         block_sum<NT, 2>(v, red, rphase);
                         if (need_d) {
                             const double est_d = sqrt(v[0] / (double)d) / P.tau1[q];
-                            r_down = 1.0 / (1.3 * pow(est_d, 1.0 / q) + 1e-6);
+                            r_down = 1.0 / (1.3 * pow(est_d, P.rq0[q]) + 1e-6);
                         }
                         if (need_u) {
                             const double est_u = sqrt(v[1] / (double)d) / P.tau3[q];
-                            r_up = 1.0 / (1.4 * pow(est_u, 1.0 / (q + 2)) + 1e-6);
+                            r_up = 1.0 / (1.4 * pow(est_u, P.rq2[q]) + 1e-6);
                         }
                     }
                     double best = r_same;
@@ -715,6 +875,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     traj_done:
         if (tid == 0) {
             s_stats[sDraws] = (long long)s_stream.n;
+            s_stats[sAttempts] += c_att;
+            s_stats[sSumQ] += c_q;
+            s_stats[sSumQQ1] += c_qq;
+            s_stats[sCorrIters] += c_it;
+            s_stats[sNfe] += c_it;
+            s_stats[sSteps] += c_steps;
             long long* so = R.stats + (size_t)row * NSTATS;
 #pragma unroll
             for (int s = 0; s < NSTATS; ++s) so[s] = s_stats[s];
@@ -725,6 +891,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         __syncthreads();
     }
 #undef GATHER
+#undef GSPMV
 #undef HORNER
 #undef RESCALE
 #undef FAIL

@@ -123,6 +123,7 @@ class RunOutput:
     grid: int
     launches: int
     count: int
+    n_failed: int = 0
 
 
 def _p(a, t=C.POINTER(C.c_double)):
@@ -233,12 +234,14 @@ class DeviceProblem:
         return RunOutput(s[:n_out].reshape(pk.n_expect, pk.n_pts),
                          s2[:n_out].reshape(pk.n_expect, pk.n_pts), vals, stats, tot, status, jc,
                          jt, ji, err, rc, out.kernel_ms, out.total_ms, out.variant, out.grid,
-                         out.launches, n)
+                         out.launches, n, int(out.n_failed))
 
 
-def _result(pk: PackedProblem, out: RunOutput, n_total: int, jumps) -> TrajectoryResult:
-    return TrajectoryResult(pk.times, out.sum / n_total, n_total, jumps, sumsq=out.sumsq,
-                            stats=stats_dict(out.stats_total))
+def _result(pk: PackedProblem, out: RunOutput, n_ok: int, jumps) -> TrajectoryResult:
+    stats = stats_dict(out.stats_total)
+    stats["failed"] = out.n_failed
+    return TrajectoryResult(pk.times, out.sum / max(n_ok, 1), n_ok, jumps, sumsq=out.sumsq,
+                            stats=stats)
 
 
 def _jump_list(out: RunOutput):
@@ -251,24 +254,32 @@ def _jump_list(out: RunOutput):
 
 def run_gpu(problem, n_total: int, master_seed: int, *, device: int = 0,
             stream: str = "philox", log_jumps: bool | None = None, max_jumps: int = 1024,
-            variant: int = -1) -> TrajectoryResult:
+            variant: int = -1, on_failure: str = "raise") -> TrajectoryResult:
     """Drop-in for ``mcwf.run_inline(problem, n_total, master_seed)``:
-    trajectories 0..n_total-1 on one GPU, count-weighted mean over them."""
+    trajectories 0..n_total-1 on one GPU, count-weighted mean over them.
+
+    ``on_failure="raise"`` (default) raises the reference's exception for
+    the lowest failing trajectory, as run_inline would; ``"exclude"``
+    averages over the trajectories that completed and reports the failures
+    in ``result.stats["failed"]``."""
     if n_total < 1:
         raise ValueError("n_total must be positive")
+    if on_failure not in ("raise", "exclude"):
+        raise ValueError("on_failure must be 'raise' or 'exclude'")
     with DeviceProblem(problem, device=device, variant=variant) as dp:
         if log_jumps is None:
             log_jumps = dp.packed.log_jumps
         out = dp.run(master_seed, 0, n_total, stream=stream,
                      max_jumps=max_jumps if log_jumps else 0, per_trajectory=log_jumps)
-        if out.rc != 0:
+        if out.rc != 0 and on_failure == "raise":
             raise_for_status(out.rc, out.error)
-        return _result(dp.packed, out, n_total, _jump_list(out) if log_jumps else None)
+        return _result(dp.packed, out, n_total - out.n_failed,
+                       _jump_list(out) if log_jumps else None)
 
 
 def run_sharded(problem, n_total: int, master_seed: int, *, rank: int, world_size: int,
                 stream: str = "philox", device: int | None = None, runner=None,
-                group=None) -> TrajectoryResult | None:
+                group=None, on_failure: str = "raise") -> TrajectoryResult | None:
     """One rank of a multi-GPU run (one process per GPU, torch.distributed
     initialised by the caller).  Rank r integrates its contiguous range of
     global trajectory indices; the per-point sums, sums of squares, counters
@@ -295,20 +306,22 @@ def run_sharded(problem, n_total: int, master_seed: int, *, rank: int, world_siz
     backend = dist.get_backend(group)
     tdev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else \
         torch.device("cpu")
-    # one float64 all-reduce: [sum | sumsq | stats]
+    # one float64 all-reduce: [sum | sumsq | stats | failed]
     buf = torch.from_numpy(np.concatenate([out.sum.ravel(), out.sumsq.ravel(),
-                                           out.stats_total.astype(np.float64)])).to(tdev)
+                                           out.stats_total.astype(np.float64),
+                                           [float(out.n_failed)]])).to(tdev)
     dist.all_reduce(buf, group=group)
     fail = torch.tensor([fail_row], dtype=torch.int64, device=tdev)
     dist.all_reduce(fail, op=dist.ReduceOp.MIN, group=group)
     first_fail = int(fail.item())
-    if first_fail != np.iinfo(np.int64).max:
+    if first_fail != np.iinfo(np.int64).max and on_failure == "raise":
         if out.rc != 0 and out.error["traj"] == first_fail:
             raise_for_status(out.rc, out.error)
         raise RuntimeError(f"trajectory {first_fail} failed on another rank")
     host = buf.cpu().numpy()
     s = host[:n_out].reshape(packed.n_expect, packed.n_pts)
     s2 = host[n_out:2 * n_out].reshape(packed.n_expect, packed.n_pts)
-    stats = host[2 * n_out:].astype(np.int64)
-    return TrajectoryResult(packed.times, s / n_total, n_total, None, sumsq=s2,
-                            stats=stats_dict(stats))
+    stats = stats_dict(host[2 * n_out:2 * n_out + native.NSTATS].astype(np.int64))
+    stats["failed"] = int(host[-1])
+    n_ok = n_total - stats["failed"]
+    return TrajectoryResult(packed.times, s / max(n_ok, 1), n_ok, None, sumsq=s2, stats=stats)

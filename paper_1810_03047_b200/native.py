@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqtm.so")
+LIB_PATH = os.environ.get("QTM_LIB") or os.path.join(HERE, "libqtm.so")
 
 ABI_VERSION = 1
 NSTATS = 16
@@ -74,7 +74,7 @@ class QtmRunOut(C.Structure):
                 ("stats_total", _I64P), ("status", _I32P), ("jump_count", _I64P),
                 ("jump_t", _F64P), ("jump_idx", _I32P), ("error", QtmError),
                 ("kernel_ms", C.c_float), ("total_ms", C.c_float), ("variant", C.c_int32),
-                ("grid", C.c_int32), ("launches", C.c_int64)]
+                ("grid", C.c_int32), ("launches", C.c_int64), ("n_failed", C.c_int64)]
 
 
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",
