@@ -212,6 +212,10 @@ def main(argv=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # the clock sampler starts before the warm-up so that nvidia-smi's own
+    # start-up is over before the timed region
+    clocks = ClockSampler(local)
+    clocks.start()
     dp = DeviceProblem(packed, device=local, variant=args.variant)
     for _ in range(args.warmup):
         out = dp.run(SEED, begin, end, resident=True, cuda_stream=stream.cuda_stream)
@@ -219,9 +223,6 @@ def main(argv=None):
             raise RuntimeError(f"warm-up run failed: {out.error}")
 
     # ---- device-timed leg: inputs resident in HBM -------------------------
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)

@@ -235,7 +235,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
-    if (n > 65536) return QTM_OK;
+    if (n > 4096) return QTM_OK;  // byte offsets col*16 must fit 16 bits
     std::vector<int> width(nslices, 0);
     for (int64_t i = 0; i < n; ++i) {
         const int len = (int)(g.row_ptr[i + 1] - g.row_ptr[i]);
@@ -254,8 +254,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         total += width[sl] * 32;
     }
     std::vector<double2> dict(1, make_double2(0.0, 0.0));
-    std::vector<double2> diag(dp, make_double2(0.0, 0.0));
-    std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: col 0, value index 0 (= 0.0)
+    std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: x[0] * dict[0] (= 0)
     struct Key {
         uint64_t a, b;
         bool operator<(const Key& o) const { return a < o.a || (a == o.a && b < o.b); }
@@ -266,33 +265,25 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         int k = 0;
         for (int64_t j = g.row_ptr[i]; j < g.row_ptr[i + 1]; ++j, ++k) {
             const double re = g.values[2 * j], im = g.values[2 * j + 1];
-            uint32_t vi;
-            if (g.col_ind[j] == i) {
-                diag[i] = make_double2(re, im);
-                vi = 0xFFFFu;
-            } else {
-                Key key;
-                memcpy(&key.a, &re, 8);
-                memcpy(&key.b, &im, 8);
-                auto it = index.find(key);
-                if (it == index.end()) {
-                    if (dict.size() >= 0xFFFEu) return QTM_OK;  // too many distinct values
-                    it = index.emplace(key, (int)dict.size()).first;
-                    dict.push_back(make_double2(re, im));
-                }
-                vi = (uint32_t)it->second;
+            Key key;
+            memcpy(&key.a, &re, 8);
+            memcpy(&key.b, &im, 8);
+            auto it = index.find(key);
+            if (it == index.end()) {
+                if (dict.size() >= 4096) return QTM_OK;  // too many distinct values
+                it = index.emplace(key, (int)dict.size()).first;
+                dict.push_back(make_double2(re, im));
             }
-            ent[off[sl] + k * 32 + lane] = (uint32_t)g.col_ind[j] | (vi << 16);
+            ent[off[sl] + k * 32 + lane] = (uint32_t)(16 * g.col_ind[j]) | ((uint32_t)(16 * it->second) << 16);
         }
     }
-    const size_t bytes = sizeof(double2) * (dict.size() + dp) + sizeof(uint32_t) * ent.size();
+    const size_t bytes = sizeof(double2) * dict.size() + sizeof(uint32_t) * ent.size();
     if (fixed_smem + bytes > smem_cap) return QTM_OK;
     uint32_t* d_ent = nullptr;
-    double2 *d_dict = nullptr, *d_diag = nullptr;
+    double2* d_dict = nullptr;
     int *d_off = nullptr, *d_w = nullptr;
     CUDA_TRY(upload(p, &d_ent, ent.data(), ent.size()));
     CUDA_TRY(upload(p, &d_dict, dict.data(), dict.size()));
-    CUDA_TRY(upload(p, &d_diag, diag.data(), (size_t)dp));
     CUDA_TRY(upload(p, &d_off, off.data(), (size_t)nslices));
     CUDA_TRY(upload(p, &d_w, width.data(), (size_t)nslices));
     DevProblem& P = p->dp;
@@ -303,9 +294,38 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
     P.sell_dict = d_dict;
     P.sell_off = d_off;
     P.sell_w = d_w;
-    P.diag = d_diag;
     p->smem = fixed_smem + bytes;
     *staged = true;
+    return QTM_OK;
+}
+
+// Dense copies of the observables that are diagonal (every stored entry on
+// the diagonal): the recording pass then reads one coalesced value per row.
+int build_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp) {
+    unsigned mask = 0;
+    std::vector<double2> dense;
+    for (int k = 0; k < d->n_expect; ++k) {
+        const qtm_csr& m = d->expect[k];
+        bool diag = true;
+        for (int64_t i = 0; i < d->dim && diag; ++i) {
+            const int64_t len = m.row_ptr[i + 1] - m.row_ptr[i];
+            if (len > 1 || (len == 1 && m.col_ind[m.row_ptr[i]] != i)) diag = false;
+        }
+        if (!diag) continue;
+        mask |= 1u << k;
+        dense.resize((size_t)(k + 1) * dp, make_double2(0.0, 0.0));
+        for (int64_t i = 0; i < d->dim; ++i)
+            if (m.row_ptr[i + 1] > m.row_ptr[i]) {
+                const int64_t j = m.row_ptr[i];
+                dense[(size_t)k * dp + i] = make_double2(m.values[2 * j], m.values[2 * j + 1]);
+            }
+    }
+    p->dp.e_diag_mask = mask;
+    if (mask) {
+        double2* dd = nullptr;
+        CUDA_TRY(upload(p, &dd, dense.data(), dense.size()));
+        p->dp.e_diag = dd;
+    }
     return QTM_OK;
 }
 
@@ -432,6 +452,7 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem,
                         (size_t)smem_cap - 1024, &staged);
     }
+    if (rc == QTM_OK) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->smem > 48 * 1024 &&
         cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap - 1024) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");

@@ -69,17 +69,20 @@ struct DevProblem {
     const double* times;
     // G in sliced-ELL form for shared-memory staging (built per kernel
     // variant on the host): slice = 32 consecutive rows, entries stored
-    // [slice][k][lane] as uint32 (col | value-index << 16), widths padded to
-    // be uniform per warp; value index 0xFFFF = the row's diagonal (kept in a
-    // register), other indices point into a dictionary of distinct values
-    // (index 0 = 0.0, used for padding).  sell_mode 0 = plain CSR via L1/L2.
+    // [slice][k][lane] as uint32 (16*col | 16*value-index << 16), widths
+    // padded to be uniform per warp; the value index points into a dictionary
+    // of the distinct entries of G (index 0 = 0.0, used for padding).
+    // sell_mode 0 = plain CSR through L1/L2 (d > 4096 or > 4095 distinct values).
     int sell_mode;
     int sell_entries, sell_dict_n;
     const uint32_t* sell_ent;
     const double2* sell_dict;
     const int* sell_off;    // [DP/32] first entry of each slice
     const int* sell_w;      // [DP/32] width of each slice
-    const double2* diag;    // [DP] diagonal of G (0 where absent)
+    // observables that are diagonal in the basis (number operators, sigma_z):
+    // bit k of e_diag_mask set => dense values at e_diag[k * DP + i]
+    unsigned e_diag_mask;
+    const double2* e_diag;
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
     // per-order constants the reference evaluates inline, tabulated on the
@@ -134,24 +137,26 @@ __device__ __forceinline__ double2 row_dot(const DevCsr& m, int i, const double2
 // f = G x for this thread's E rows from the staged sliced-ELL copy: the E
 // rows' chains are interleaved for ILP; each row is still summed in column
 // order (entries k ascending), so the rounding matches row_dot exactly.
+// Entry = x byte offset (col*16, low half) | dictionary byte offset (high
+// half), so each entry costs two 16-byte shared loads and no index math.
 template <int NT, int E>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
-                                          const double2* __restrict__ dict,
-                                          const double2* __restrict__ diag, const int (&off)[E],
+                                          const double2* __restrict__ dict, const int (&off)[E],
                                           int width, const double2* __restrict__ x,
                                           double2 (&out)[E]) {
     const int lane = threadIdx.x & 31;
+    const char* const xb = reinterpret_cast<const char*>(x);
+    const char* const db = reinterpret_cast<const char*>(dict);
     double sr[E], si[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
-#pragma unroll 4
+#pragma unroll 2
     for (int k = 0; k < width; ++k) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             const uint32_t u = ent[off[e] + k * 32 + lane];
-            const unsigned vi = u >> 16;
-            const double2 v = vi == 0xFFFFu ? diag[threadIdx.x + NT * e] : dict[vi];
-            const double2 xv = x[u & 0xFFFFu];
+            const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
+            const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
             sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
             si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
         }
@@ -183,9 +188,18 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& phas
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            double s = lane < NW ? buf[k * NW + lane] : 0.0;
+            double s;
+            if constexpr ((NW & (NW - 1)) == 0) {
+                // power-of-two warp count: every lane loads partial lane % NW,
+                // log2(NW) butterfly levels leave the total in all lanes
+                s = buf[k * NW + (lane & (NW - 1))];
 #pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+                for (int m = NW / 2; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+            } else {
+                s = lane < NW ? buf[k * NW + lane] : 0.0;
+#pragma unroll
+                for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+            }
             v[k] = s;
         }
         phase ^= 1;
@@ -450,12 +464,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     // ---- stage G (sliced ELL + value dictionary) in shared memory once
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
                                                        TrajKernel<NT, E, RREG>::smem_bytes());
-    double2* const s_diag = s_dict + P.sell_dict_n;
-    uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_diag + DP);
+    uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_dict + P.sell_dict_n);
     int goff[E], gwidth = 0;
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
-        for (int i = tid; i < DP; i += NT) s_diag[i] = P.diag[i];
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
         const int warp = tid >> 5;
 #pragma unroll
@@ -467,7 +479,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV(xs, f)                                                         \
     do {                                                                     \
         if (P.sell_mode) {                                                   \
-            sell_spmv<NT, E>(s_ent, s_dict, s_diag, goff, gwidth, (xs), f);  \
+            sell_spmv<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f);          \
         } else {                                                             \
             _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
                 f[e] = act[e] ? row_dot(P.g, ii[e], (xs)) : make_double2(0.0, 0.0); \
@@ -551,8 +563,16 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             for (int kk = 0; kk < KRED - 1; ++kk) {                          \
                 const int k = k0 + kk;                                       \
                 if (k < P.ne) {                                              \
+                    const bool dg__ = (P.e_diag_mask >> k) & 1u;             \
                     _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) { \
-                        const double2 s = row_dot(P.e[k], ii[e], xs__);      \
+                        double2 s;                                           \
+                        if (dg__) {                                          \
+                            const double2 ev__ = P.e_diag[(size_t)k * DP + ii[e]]; \
+                            s = make_double2(0.0 + (ev__.x * psi[e].x - ev__.y * psi[e].y), \
+                                             0.0 + (ev__.x * psi[e].y + ev__.y * psi[e].x)); \
+                        } else {                                             \
+                            s = row_dot(P.e[k], ii[e], xs__);                \
+                        }                                                    \
                         v__[kk] += psi[e].x * s.x - (-psi[e].y) * s.y;       \
                     }                                                        \
                 }                                                            \
