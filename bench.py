@@ -167,7 +167,8 @@ def main(argv=None):
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
-    ap.add_argument("--variant", type=int, default=-1)
+    ap.add_argument("--variant", type=int, default=-2,
+                    help="kernel variant (-1: by dimension, -2: autotune during warm-up)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--trajectories", type=int, default=0,
                     help="override the config's trajectory count (exploration only)")
@@ -186,8 +187,8 @@ def main(argv=None):
 
     from paper_1810_03047_b200 import configs, native
     from paper_1810_03047_b200.configs import N_TRAJECTORIES
-    from paper_1810_03047_b200.engine import (DeviceProblem, bytes_model, flops_model,
-                                              run_sharded, shard_range, stats_dict)
+    from paper_1810_03047_b200.engine import (DeviceProblem, autotune_variant, bytes_model,
+                                              flops_model, run_sharded, shard_range, stats_dict)
     from paper_1810_03047_b200.packing import pack_problem
 
     torch.cuda.set_device(local)
@@ -216,6 +217,8 @@ def main(argv=None):
     # start-up is over before the timed region
     clocks = ClockSampler(local)
     clocks.start()
+    if args.variant == -2:  # untimed: choose the kernel variant on a sample
+        args.variant = autotune_variant(packed, device=local)
     dp = DeviceProblem(packed, device=local, variant=args.variant)
     for _ in range(args.warmup):
         out = dp.run(SEED, begin, end, resident=True, cuda_stream=stream.cuda_stream)

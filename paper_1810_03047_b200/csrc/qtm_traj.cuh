@@ -22,7 +22,7 @@
 // Differences from the reference are rounding-level only: block reductions
 // are tree sums (the reference sums sequentially), the predicted history is
 // undone in place on a rejected attempt instead of kept in a second copy,
-// and hypot/pow come from CUDA's libdevice.
+// and hypot/pow come from CUDA's libdevice (the reference: glibc libm).
 #pragma once
 #include <cstdint>
 
@@ -150,7 +150,7 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
     double sr[E], si[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
-#pragma unroll 2
+#pragma unroll (E >= 4 ? 1 : 2)
     for (int k = 0; k < width; ++k) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -215,7 +215,11 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& phas
 template <int RREG, int E, int DP>
 struct Hist {
     using Z = double2[RREG][E];
-    using O = double2* [E];
+    // this thread's overflow column: row j >= RREG of component e
+    struct O {
+        double2* p;
+        __device__ __forceinline__ double2& at(int j, int e) const { return p[(j - RREG) * DP + e * (DP / E)]; }
+    };
 
     // ---- order-specialised register paths (q + 1 <= RREG): straight-line
     // code, no per-row guards.  Dispatch by switch on the uniform order.
@@ -286,7 +290,7 @@ struct Hist {
     // ---- general paths (any q; rows >= RREG in the overflow column)
     // zp = Pascal(z) in place, passes r = 0..q-1, j = q-1 down to r
     // (_kernels.py:133-137)
-    __device__ __forceinline__ static void predict(Z& z, O& ovf, int q) {
+    __device__ __forceinline__ static void predict(Z& z, const O& ovf, int q) {
 #define CALL_(Q) predict_q<Q>(z)
         QTM_QSWITCH(CALL_)
 #undef CALL_
@@ -294,11 +298,11 @@ struct Hist {
             for (int j = q - 1; j >= (r > RREG ? r : RREG); --j) {
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    ovf[e][(j - RREG) * DP] = cadd(ovf[e][(j - RREG) * DP], ovf[e][(j + 1 - RREG) * DP]);
+                    ovf.at(j, e) = cadd(ovf.at(j, e), ovf.at(j + 1, e));
             }
             if (RREG - 1 >= r && RREG - 1 < q) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) z[RREG - 1][e] = cadd(z[RREG - 1][e], ovf[e][0]);
+                for (int e = 0; e < E; ++e) z[RREG - 1][e] = cadd(z[RREG - 1][e], ovf.at(RREG, e));
             }
 #pragma unroll
             for (int j = RREG - 2; j >= 0; --j) {
@@ -311,7 +315,7 @@ struct Hist {
     }
 
     // inverse of predict (rejected attempt): passes r = q-1..0, j = r..q-1
-    __device__ __forceinline__ static void undo(Z& z, O& ovf, int q) {
+    __device__ __forceinline__ static void undo(Z& z, const O& ovf, int q) {
 #define CALL_(Q) undo_q<Q>(z)
         QTM_QSWITCH(CALL_)
 #undef CALL_
@@ -325,19 +329,19 @@ struct Hist {
             }
             if (RREG - 1 >= r && RREG - 1 < q) {
 #pragma unroll
-                for (int e = 0; e < E; ++e) z[RREG - 1][e] = csub(z[RREG - 1][e], ovf[e][0]);
+                for (int e = 0; e < E; ++e) z[RREG - 1][e] = csub(z[RREG - 1][e], ovf.at(RREG, e));
             }
             for (int j = (r > RREG ? r : RREG); j < q; ++j) {
 #pragma unroll
                 for (int e = 0; e < E; ++e)
-                    ovf[e][(j - RREG) * DP] = csub(ovf[e][(j - RREG) * DP], ovf[e][(j + 1 - RREG) * DP]);
+                    ovf.at(j, e) = csub(ovf.at(j, e), ovf.at(j + 1, e));
             }
         }
     }
 
     // z[j] *= ratio^j, j = 1..q, ratio^j by repeated multiplication
     // (nordsieck_rescale, _kernels.py:107-114)
-    __device__ __forceinline__ static void rescale(Z& z, O& ovf, int q, double ratio) {
+    __device__ __forceinline__ static void rescale(Z& z, const O& ovf, int q, double ratio) {
 #define CALL_(Q) rescale_q<Q>(z, ratio)
         QTM_QSWITCH(CALL_)
 #undef CALL_
@@ -353,12 +357,12 @@ struct Hist {
         for (int j = RREG; j <= q; ++j) {
             f *= ratio;
 #pragma unroll
-            for (int e = 0; e < E; ++e) ovf[e][(j - RREG) * DP] = cscale(f, ovf[e][(j - RREG) * DP]);
+            for (int e = 0; e < E; ++e) ovf.at(j, e) = cscale(f, ovf.at(j, e));
         }
     }
 
     // z[j] += l_j e, j = 0..q (_kernels.py:187-191)
-    __device__ __forceinline__ static void commit(Z& z, O& ovf, int q, const double* l,
+    __device__ __forceinline__ static void commit(Z& z, const O& ovf, int q, const double* l,
                                                   const double2 (&ev)[E]) {
 #define CALL_(Q) commit_q<Q>(z, l, ev)
         QTM_QSWITCH(CALL_)
@@ -374,26 +378,26 @@ struct Hist {
         for (int j = RREG; j <= q; ++j) {
             const double lj = l[j];
 #pragma unroll
-            for (int e = 0; e < E; ++e) ovf[e][(j - RREG) * DP] = cadd(ovf[e][(j - RREG) * DP], cscale(lj, ev[e]));
+            for (int e = 0; e < E; ++e) ovf.at(j, e) = cadd(ovf.at(j, e), cscale(lj, ev[e]));
         }
     }
 
-    __device__ __forceinline__ static double2 row(const Z& z, O& ovf, int j, int e) {
-        if (j >= RREG) return ovf[e][(j - RREG) * DP];
+    __device__ __forceinline__ static double2 row(const Z& z, const O& ovf, int j, int e) {
+        if (j >= RREG) return ovf.at(j, e);
         double2 out = z[0][e];
 #pragma unroll
         for (int jj = 1; jj < RREG; ++jj) if (jj == j) out = z[jj][e];
         return out;
     }
 
-    __device__ __forceinline__ static void set_row(Z& z, O& ovf, int j, int e, double2 v) {
-        if (j >= RREG) { ovf[e][(j - RREG) * DP] = v; return; }
+    __device__ __forceinline__ static void set_row(Z& z, const O& ovf, int j, int e, double2 v) {
+        if (j >= RREG) { ovf.at(j, e) = v; return; }
 #pragma unroll
         for (int jj = 0; jj < RREG; ++jj) if (jj == j) z[jj][e] = v;
     }
 
     // psi(s) = Horner over rows q..0 (nordsieck_eval, _kernels.py:61-69)
-    __device__ __forceinline__ static void horner(const Z& z, O& ovf, int q, double s, double2 (&out)[E]) {
+    __device__ __forceinline__ static void horner(const Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
 #define CALL_(Q) horner_q<Q>(z, s, out)
         QTM_QSWITCH(CALL_)
 #undef CALL_
@@ -401,7 +405,7 @@ struct Hist {
         for (int e = 0; e < E; ++e) out[e] = row(z, ovf, q, e);
         for (int j = q - 1; j >= RREG; --j) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) out[e] = cadd(cscale(s, out[e]), ovf[e][(j - RREG) * DP]);
+            for (int e = 0; e < E; ++e) out[e] = cadd(cscale(s, out[e]), ovf.at(j, e));
         }
 #pragma unroll
         for (int j = RREG - 1; j >= 0; --j) {
@@ -452,14 +456,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     const int tid = threadIdx.x;
     const int d = P.d;
     const int npts = P.n_pts;
-    int ii[E];
-    bool act[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) { ii[e] = tid + NT * e; act[e] = ii[e] < d; }
-    double2* ovf[E];  // this thread's overflow column, row j at ovf[e][(j - RREG) * DP]
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-        ovf[e] = (RREG < LROWS) ? R.zovf + (size_t)blockIdx.x * (LROWS - RREG) * DP + ii[e] : nullptr;
+    // component e of this thread is state index II(e); ACT(e): inside the state
+#define II(e) (tid + NT * (e))
+#define ACT(e) (II(e) < d)
+    // overflow column of this thread (rows >= RREG), rebuilt where used so it
+    // holds no register across the hot loop
+#define OVF() (typename H::O{R.zovf + (size_t)blockIdx.x * (LROWS - RREG) * DP + tid})
 
     // ---- stage G (sliced ELL + value dictionary) in shared memory once
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
@@ -482,7 +484,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             sell_spmv<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f);          \
         } else {                                                             \
             _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
-                f[e] = act[e] ? row_dot(P.g, ii[e], (xs)) : make_double2(0.0, 0.0); \
+                f[e] = ACT(e) ? row_dot(P.g, II(e), (xs)) : make_double2(0.0, 0.0); \
         }                                                                    \
     } while (0)
 
@@ -515,18 +517,18 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 // publish x[E] as the next gather buffer (write, barrier); yields `xs`
 #define GATHER(xsrc, xs)                                                     \
     double2* const xs = gath + (gbuf ^ 1) * DP;                              \
-    _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) xs[ii[e]] = (xsrc)[e]; \
+    _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) xs[II(e)] = (xsrc)[e]; \
     __syncthreads();                                                         \
     gbuf ^= 1;
 
 // Horner evaluation of the history polynomial at s into out[E]
-#define HORNER(s_, out) H::horner(z, ovf, q, (s_), out)
+#define HORNER(s_, out) H::horner(z, OVF(), q, (s_), out)
 
 // z[j] *= ratio^j for j = 1..q, h *= ratio (nordsieck_rescale + _rescale)
 #define RESCALE(ratio_)                                                      \
     do {                                                                     \
         const double rr__ = (ratio_);                                        \
-        H::rescale(z, ovf, q, rr__);                                         \
+        H::rescale(z, OVF(), q, rr__);                                         \
         h *= rr__;                                                           \
         has_eprev = false;                                                   \
         ialth = q + 1;                                                       \
@@ -557,21 +559,21 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     do {                                                                     \
         GATHER(psi, xs__);                                                   \
         double nrm__ = 0.0;                                                  \
-        _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) nrm__ += cabs2(psi[e]); \
+        _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) nrm__ += cabs2(psi[e]); \
         for (int k0 = 0; k0 < P.ne; k0 += KRED - 1) {                        \
             double v__[KRED] = {0.0, 0.0, 0.0, nrm__};                       \
             for (int kk = 0; kk < KRED - 1; ++kk) {                          \
                 const int k = k0 + kk;                                       \
                 if (k < P.ne) {                                              \
                     const bool dg__ = (P.e_diag_mask >> k) & 1u;             \
-                    _Pragma("unroll") for (int e = 0; e < E; ++e) if (act[e]) { \
+                    _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) { \
                         double2 s;                                           \
                         if (dg__) {                                          \
-                            const double2 ev__ = P.e_diag[(size_t)k * DP + ii[e]]; \
+                            const double2 ev__ = P.e_diag[(size_t)k * DP + II(e)]; \
                             s = make_double2(0.0 + (ev__.x * psi[e].x - ev__.y * psi[e].y), \
                                              0.0 + (ev__.x * psi[e].y + ev__.y * psi[e].x)); \
                         } else {                                             \
-                            s = row_dot(P.e[k], ii[e], xs__);                \
+                            s = row_dot(P.e[k], II(e), xs__);                \
                         }                                                    \
                         v__[kk] += psi[e].x * s.x - (-psi[e].y) * s.y;       \
                     }                                                        \
@@ -599,7 +601,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             z[0][e] = (y0)[e];                                               \
             z[1][e] = cscale(h, f__[e]);                                     \
             _Pragma("unroll") for (int j = 2; j < RREG; ++j) z[j][e] = make_double2(0.0, 0.0); \
-            w[e] = act[e] ? 1.0 / (P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
+            w[e] = ACT(e) ? 1.0 / (P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
         }                                                                    \
         crate = 0.7; ialth = 2; has_eprev = false;                           \
     } while (0)
@@ -609,7 +611,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         {
             double2 psi[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) psi[e] = act[e] ? P.psi0[ii[e]] : make_double2(0.0, 0.0);
+            for (int e = 0; e < E; ++e) psi[e] = ACT(e) ? P.psi0[II(e)] : make_double2(0.0, 0.0);
             RECORD(psi, 0);  // record(0) from psi0
             double r;
             DRAW(r);
@@ -628,7 +630,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     c_qq += q * (q + 1);
                     if (q + 1 > RREG) STAT(sOverflow, 1);
                     // predict: in-place Pascal triangle (_kernels.py:133-137)
-                    H::predict(z, ovf, q);
+                    H::predict(z, OVF(), q);
                     // functional corrector (_kernels.py:139-174).  The iterate
                     // lives in the gather buffers: iteration m reads gath[gbuf]
                     // and writes its update into gath[gbuf^1], which the
@@ -653,17 +655,17 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         GSPMV(cur, fg);
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
-                            if (act[e]) {
+                            if (ACT(e)) {
                                 const double2 f = fg[e];
                                 const double2 z1 = z[1][e], z0 = z[0][e];
                                 const double2 ei = csub(cscale(h, f), z1);
                                 const double2 yn = cadd(z0, cscale(l0, ei));
-                                const double2 dd = csub(yn, cur[ii[e]]);
+                                const double2 dd = csub(yn, cur[II(e)]);
                                 v[0] += cabs2(dd) * w[e] * w[e];
                                 v[1] += cabs2(ei) * w[e] * w[e];
                                 v[2] += cabs2(yn);
-                                nxt[ii[e]] = yn;
-                                ecurp[ii[e]] = ei;
+                                nxt[II(e)] = yn;
+                                ecurp[II(e)] = ei;
                             }
                         }
                         block_sum<NT, 3>(v, red, rphase);
@@ -687,13 +689,13 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                             // commit zp[j] += l_j e (_kernels.py:187-191)
                             double2 evr[E];
 #pragma unroll
-                            for (int e = 0; e < E; ++e) evr[e] = act[e] ? ecurp[ii[e]] : make_double2(0.0, 0.0);
-                            H::commit(z, ovf, q, P.l[q], evr);
+                            for (int e = 0; e < E; ++e) evr[e] = ACT(e) ? ecurp[II(e)] : make_double2(0.0, 0.0);
+                            H::commit(z, OVF(), q, P.l[q], evr);
                             break;  // accepted
                         }
                     }
                     // rejected attempt: restore the un-predicted history
-                    H::undo(z, ovf, q);
+                    H::undo(z, OVF(), q);
                     if (!converged) {
                         STAT(sCorrFail, 1);
                         if (++ncf >= 10) FAIL(kErrCorrector);
@@ -730,7 +732,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = z[0][e];
-                    w[e] = act[e] ? 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
+                    w[e] = ACT(e) ? 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
                 }
                 ialth -= 1;
                 if (ialth == 0) {
@@ -745,9 +747,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         const double2* const epp = ebuf + (ecur ^ 1) * DP;
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
-                            if (act[e]) {
-                                const double2 zq = H::row(z, ovf, q, e);
-                                const double2 de = csub(ecp[ii[e]], epp[ii[e]]);
+                            if (ACT(e)) {
+                                const double2 zq = H::row(z, OVF(), q, e);
+                                const double2 de = csub(ecp[II(e)], epp[II(e)]);
                                 v[0] += cabs2(zq) * w[e] * w[e];
                                 v[1] += cabs2(de) * w[e] * w[e];
                             }
@@ -775,7 +777,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                             const double2* const ecp = ebuf + ecur * DP;
 #pragma unroll
                             for (int e = 0; e < E; ++e)
-                                H::set_row(z, ovf, q + 1, e, act[e] ? cscale(cu, ecp[ii[e]]) : make_double2(0.0, 0.0));
+                                H::set_row(z, OVF(), q + 1, e, ACT(e) ? cscale(cu, ecp[II(e)]) : make_double2(0.0, 0.0));
                             q = q + 1;
                             STAT(sOrderUp, 1);
                         } else if (best == r_down) {
@@ -800,7 +802,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         HORNER((t_lo - t) / h, a1);
                         HORNER((t - t) / h, a2);
 #pragma unroll
-                        for (int e = 0; e < E; ++e) if (act[e]) { v2[0] += cabs2(a1[e]); v2[1] += cabs2(a2[e]); }
+                        for (int e = 0; e < E; ++e) if (ACT(e)) { v2[0] += cabs2(a1[e]); v2[1] += cabs2(a2[e]); }
                     }
                     block_sum<NT, 2>(v2, red, rphase);
                     const double f_lo = v2[0], f_hi = v2[1];
@@ -823,7 +825,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 double2 am[E];
                                 HORNER((mid - t) / h, am);
 #pragma unroll
-                                for (int e = 0; e < E; ++e) if (act[e]) v1[0] += cabs2(am[e]);
+                                for (int e = 0; e < E; ++e) if (ACT(e)) v1[0] += cabs2(am[e]);
                             }
                             block_sum<NT, 1>(v1, red, rphase);
                             STAT(sBisect, 1);
@@ -852,7 +854,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 if (c0 + kk < P.nc) {
 #pragma unroll
                                     for (int e = 0; e < E; ++e)
-                                        if (act[e]) v4[kk] += cabs2(row_dot(P.c[c0 + kk], ii[e], xs));
+                                        if (ACT(e)) v4[kk] += cabs2(row_dot(P.c[c0 + kk], II(e), xs));
                                 }
                             }
                             block_sum<NT, KRED>(v4, red, rphase);
@@ -871,7 +873,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         const double scl = 1.0 / sqrt(wts[idx]);
 #pragma unroll
                         for (int e = 0; e < E; ++e)
-                            pst[e] = act[e] ? cscale(scl, row_dot(P.c[idx], ii[e], xs)) : make_double2(0.0, 0.0);
+                            pst[e] = ACT(e) ? cscale(scl, row_dot(P.c[idx], II(e), xs)) : make_double2(0.0, 0.0);
                         if (tid == 0 && njumps < R.max_jumps) {
                             R.jump_t[(size_t)row * R.max_jumps + njumps] = ts;
                             R.jump_idx[(size_t)row * R.max_jumps + njumps] = idx;
@@ -910,6 +912,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         }
         __syncthreads();
     }
+#undef OVF
+#undef II
+#undef ACT
 #undef GATHER
 #undef GSPMV
 #undef HORNER

@@ -32,7 +32,8 @@ from .packing import PackedProblem, pack_problem
 from .problem import OdeFailure, TrajectoryResult
 
 __all__ = ["DeviceProblem", "RunOutput", "run_gpu", "run_sharded", "partition_trajectories",
-           "raise_for_status", "stats_dict", "flops_model"]
+           "raise_for_status", "stats_dict", "flops_model", "autotune_variant",
+           "candidate_variants"]
 
 
 def partition_trajectories(n_total: int, n_workers: int) -> list[int]:
@@ -235,6 +236,44 @@ class DeviceProblem:
                          s2[:n_out].reshape(pk.n_expect, pk.n_pts), vals, stats, tot, status, jc,
                          jt, ji, err, rc, out.kernel_ms, out.total_ms, out.variant, out.grid,
                          out.launches, n, int(out.n_failed))
+
+
+_TUNED: dict = {}
+
+
+def candidate_variants(dim: int) -> list[int]:
+    """Kernel variants able to hold a state of this dimension without
+    wasting more than half of their lanes (the smallest fit always counts)."""
+    vs = native.variants()
+    fits = [i for i, (t, e, _) in enumerate(vs) if t * e >= dim]
+    if not fits:
+        return []
+    smallest = min(vs[i][0] * vs[i][1] for i in fits)
+    return [i for i in fits if vs[i][0] * vs[i][1] <= max(2 * dim, smallest)]
+
+
+def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | None = None,
+                     seed: int = 987654321) -> int:
+    """Pick the fastest kernel variant for this problem by timing each
+    candidate on a sample of trajectories (result cached per problem digest
+    and device).  The register budget for the Nordsieck history is the main
+    trade-off: enough rows for the orders the problem actually reaches, but
+    no more than needed to keep more warps resident."""
+    key = (packed.digest, device)
+    if key in _TUNED:
+        return _TUNED[key]
+    cands = candidate_variants(packed.dim)
+    if len(cands) <= 1:
+        _TUNED[key] = cands[0] if cands else -1
+        return _TUNED[key]
+    best, best_ms = -1, float("inf")
+    for v in cands:
+        with DeviceProblem(packed, device=device, variant=v) as dp:
+            out = dp.run(seed, 0, sample or 512, resident=True)
+        if out.kernel_ms < best_ms:
+            best, best_ms = v, out.kernel_ms
+    _TUNED[key] = best
+    return best
 
 
 def _result(pk: PackedProblem, out: RunOutput, n_ok: int, jumps) -> TrajectoryResult:
