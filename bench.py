@@ -56,29 +56,79 @@ def _env_int(name, default):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region.
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML is polled from a background thread (every 250 ms) instead of an
+    nvidia-smi subprocess: the subprocess's own queries were measured to stall
+    the GPU work of this process by ~100 ms per sample on the B200 pool.
+    QTM_CLOCKS=smi selects the nvidia-smi sampler, QTM_CLOCKS=off disables."""
 
-    def __init__(self, device: int):
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, device: int, interval: float = 0.25):
         self.device = device
+        self.interval = interval
+        self.mode = os.environ.get("QTM_CLOCKS", "nvml")
+        self.samples = []
+        self._stop = None
+        self._thread = None
         self.proc = None
         self.path = None
 
     def start(self):
+        if self.mode == "off":
+            return
+        if self.mode == "smi":
+            return self._start_smi()
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            return self._start_smi()
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, smax, rs))
+                except Exception:
+                    pass
+                self._stop.wait(self.interval)
+
+        self._thread = threading.Thread(target=loop, daemon=True)
+        self._thread.start()
+
+    def _start_smi(self):
+        query = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={query}",
                  "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
                 stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
 
     def stop(self):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
+            if not self.samples:
+                return None
+            names = [n for n, bit in self.REASONS.items()
+                     if any(rs & bit for _, _, rs in self.samples)]
+            return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
+                    "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": sorted(names),
+                    "samples": len(self.samples), "source": "nvml"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -103,7 +153,7 @@ class ClockSampler:
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "source": "nvidia-smi"}
 
 
 def cpu_reference(packed, sample: int, steps: int, warmup: int, threads: int):
@@ -234,17 +284,23 @@ def main(argv=None):
     kernel_ms = []
     launches = 0
     outs = []
+    step_ev = []
     for _ in range(args.steps):
         flush.zero_()
+        e_a = torch.cuda.Event(enable_timing=True)
+        e_a.record(stream)
         out = dp.run(SEED, begin, end, resident=True, cuda_stream=stream.cuda_stream)
         kernel_ms.append(out.kernel_ms)
         launches += out.launches
         outs.append(out)
+        step_ev.append(e_a)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     step_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    per_step = [step_ev[i].elapsed_time(step_ev[i + 1] if i + 1 < len(step_ev) else ev1)
+                for i in range(len(step_ev))]
     n_failed = int(_sum_over_ranks(dist, torch, local, outs[-1].n_failed, world))
     # completed trajectories per second (a trajectory on which the reference
     # controller itself collapses -- OdeFailure -5 -- is excluded)
@@ -319,6 +375,7 @@ def main(argv=None):
                          "hbm_equiv_gbs": hbm_equiv,
                          "hbm_equiv_note": "state-streaming model bytes (SURVEY §8d) / kernel "
                                            "time; the kernel keeps state on chip"},
+            "step_ms": [round(x, 3) for x in per_step],
             "work": {k: st[k] for k in ("attempts", "steps", "corr_iters", "jumps",
                                         "corr_fail", "err_reject", "overflow_attempts")},
             "clocks": clk,

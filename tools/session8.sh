@@ -1,0 +1,3 @@
+cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+bash tools/capture_profiles.sh r01
