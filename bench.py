@@ -174,13 +174,14 @@ def cpu_reference(packed, sample: int, steps: int, warmup: int, threads: int):
     return done / (sum(times) / len(times)), sum(times) / len(times)
 
 
-CPU_SAMPLE_PER_THREAD = {"c1": 64, "c2": 16, "c3": 8, "c4": 2, "c5": 1}
+CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1}
 
 
 def _sum_over_ranks(dist, torch, local, x, world):
     if world == 1:
         return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
     dist.all_reduce(t)
     return float(t.item())
 
@@ -241,9 +242,17 @@ def main(argv=None):
                                               flops_model, run_sharded, shard_range, stats_dict)
     from paper_1810_03047_b200.packing import pack_problem
 
+    n_dev = torch.cuda.device_count()
+    if local >= n_dev:  # more ranks than GPUs (functional test of the multi-rank path only)
+        local = local % n_dev
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if n_dev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            # NCCL refuses two ranks on one GPU; the tiny end-of-run reduction
+            # then goes through gloo (never the case on an 8-GPU box)
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream(local)
     problem = configs.build(args.config)
     packed = pack_problem(problem)
@@ -259,7 +268,8 @@ def main(argv=None):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -271,6 +281,7 @@ def main(argv=None):
         args.variant = autotune_variant(packed, device=local)
     dp = DeviceProblem(packed, device=local, variant=args.variant)
     for _ in range(args.warmup):
+        flush.zero_()  # also loads the fill kernel's module before timing (lazy loading)
         out = dp.run(SEED, begin, end, resident=True, cuda_stream=stream.cuda_stream)
         if out.rc not in (0, -1, -4, -5, -6):  # trajectory failures are the reference's own
             raise RuntimeError(f"warm-up run failed: {out.error}")
