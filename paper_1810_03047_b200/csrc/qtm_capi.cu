@@ -46,6 +46,33 @@ __global__ void ensemble_partial(const double* __restrict__ values, const int* _
     psq[c * n_out + o] = s2;
 }
 
+// per-trajectory values from the per-warp partial sums the trajectory
+// kernel stored: value = (sum_w num_w) / (sum_w nrm_w), warps in order;
+// a zero norm fails the trajectory like record_expectation (trajectory.py:126-127)
+__global__ void finalize_records(const double* __restrict__ part, int* __restrict__ status,
+                                 double* __restrict__ values, long long n_traj, int n_pts, int ne,
+                                 int nw, unsigned long long* __restrict__ first_fail) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_traj * n_pts) return;
+    const long long row = idx / n_pts;
+    const int gi = (int)(idx % n_pts);
+    const double* p = part + idx * (long long)(ne + 1) * nw;
+    double nrm = 0.0;
+    for (int w = 0; w < nw; ++w) nrm += p[(long long)ne * nw + w];
+    if (nrm == 0.0) {
+        if (status[row] == 0) {
+            status[row] = kErrZeroVector;
+            atomicMin(first_fail, (unsigned long long)row);
+        }
+        return;
+    }
+    for (int k = 0; k < ne; ++k) {
+        double num = 0.0;
+        for (int w = 0; w < nw; ++w) num += p[(long long)k * nw + w];
+        values[(row * ne + k) * n_pts + gi] = num / nrm;
+    }
+}
+
 __global__ void ensemble_final(const double* __restrict__ psum, const double* __restrict__ psq,
                                int n_chunks, int n_out, double* __restrict__ sum,
                                double* __restrict__ sumsq) {
@@ -78,6 +105,7 @@ __global__ void stats_total(const long long* __restrict__ stats, const int* __re
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long g_phase_cycles[16];  // last run's phase counters (QTM_PHASES builds)
 
 int set_error(int code, const std::string& msg) {
     g_last_error = msg;
@@ -177,11 +205,11 @@ struct qtm_problem {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // run scratch (grown on demand, reused across calls)
-    DevBuf<double> values, err, err_r, psum, psq, sum, sumsq, jump_t, script;
+    DevBuf<double> values, rec_partial, err, err_r, psum, psq, sum, sumsq, jump_t, script;
     DevBuf<long long> stats, jump_count, script_len, stats_tot;
     DevBuf<int> status, jump_idx;
     DevBuf<double2> zovf;
-    DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row
+    DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row, [2..17] phases
     std::mutex mu;
 };
 
@@ -321,6 +349,7 @@ int build_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp) {
             }
     }
     p->dp.e_diag_mask = mask;
+    p->dp.e_need_gather = d->n_expect > 0 && mask != ((d->n_expect >= 32) ? 0xFFFFFFFFu : ((1u << d->n_expect) - 1u));
     if (mask) {
         double2* dd = nullptr;
         CUDA_TRY(upload(p, &dd, dense.data(), dense.size()));
@@ -334,7 +363,7 @@ void free_problem(qtm_problem* p) {
     cudaSetDevice(p->device);
     cudaStream_t s = p->stream;
     for (void* a : p->allocs) cudaFreeAsync(a, s);
-    p->values.release(s); p->err.release(s); p->err_r.release(s); p->psum.release(s); p->psq.release(s);
+    p->values.release(s); p->rec_partial.release(s); p->err.release(s); p->err_r.release(s); p->psum.release(s); p->psq.release(s);
     p->sum.release(s); p->sumsq.release(s); p->jump_t.release(s); p->script.release(s);
     p->stats.release(s); p->jump_count.release(s); p->script_len.release(s); p->stats_tot.release(s);
     p->status.release(s); p->jump_idx.release(s); p->zovf.release(s); p->ctl.release(s);
@@ -456,7 +485,7 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (rc == QTM_OK && p->smem > 48 * 1024 &&
         cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap - 1024) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
-    if (rc == QTM_OK && p->ctl.ensure(2, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
+    if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
     if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "problem upload failed");
     if (rc != QTM_OK) {
@@ -502,6 +531,8 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     o->grid = (int32_t)grid;
 
     CUDA_TRY(p->values.ensure((size_t)count * std::max(n_out, 1), s));
+    const int nw = var.threads / 32;
+    CUDA_TRY(p->rec_partial.ensure((size_t)count * p->n_pts * (p->n_expect + 1) * nw, s));
     CUDA_TRY(p->stats.ensure((size_t)count * QTM_NSTATS, s));
     CUDA_TRY(p->status.ensure(count, s));
     CUDA_TRY(p->err.ensure((size_t)count * 4, s));
@@ -526,7 +557,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         CUDA_TRY(cudaMemcpyAsync(p->script_len.p, a->script_len, sizeof(int64_t) * count,
                                  cudaMemcpyHostToDevice, s));
     }
-    const unsigned long long ctl_init[2] = {0ull, ~0ull};
+    unsigned long long ctl_init[18] = {0ull, ~0ull};
     CUDA_TRY(cudaEventRecord(p->ev[0], s));
     CUDA_TRY(cudaMemcpyAsync(p->ctl.p, ctl_init, sizeof(ctl_init), cudaMemcpyHostToDevice, s));
 
@@ -540,6 +571,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     R.script_stride = a->script_stride;
     R.script_fallback = a->script_fallback;
     R.values = p->values.p;
+    R.rec_partial = p->rec_partial.p;
     R.stats = p->stats.p;
     R.status = p->status.p;
     R.err = p->err.p;
@@ -551,12 +583,19 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     R.zovf = p->zovf.p;
     R.counter = p->ctl.p;
     R.first_fail = p->ctl.p + 1;
+    R.phase_cycles = p->ctl.p + 2;
     void* kargs[] = {(void*)&p->dp, (void*)&R};
     CUDA_TRY(cudaEventRecord(p->ev[1], s));
     CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)grid), dim3(var.threads), kargs, p->smem, s));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev[2], s));
     int64_t launches = 1;
+    {
+        const long long cells = count * p->n_pts;
+        finalize_records<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
+            p->rec_partial.p, p->status.p, p->values.p, count, (int)p->n_pts, p->n_expect, nw, p->ctl.p + 1);
+        launches += 1;
+    }
     if (n_out > 0) {
         dim3 g1((n_out + 127) / 128, n_chunks);
         ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, p->status.p, count, n_out, chunk, p->psum.p, p->psq.p);
@@ -572,7 +611,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         CUDA_TRY(cudaMemcpyAsync(o->sum, p->sum.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
         if (o->sumsq) CUDA_TRY(cudaMemcpyAsync(o->sumsq, p->sumsq.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
     }
-    unsigned long long ctl_out[2];
+    unsigned long long ctl_out[18];
     CUDA_TRY(cudaMemcpyAsync(ctl_out, p->ctl.p, sizeof(ctl_out), cudaMemcpyDeviceToHost, s));
     long long tot_host[QTM_NSTATS + 1];
     CUDA_TRY(cudaMemcpyAsync(tot_host, p->stats_tot.p, sizeof(tot_host), cudaMemcpyDeviceToHost, s));
@@ -596,6 +635,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     o->launches = launches;
     if (o->stats_total) memcpy(o->stats_total, tot_host, sizeof(int64_t) * QTM_NSTATS);
     o->n_failed = tot_host[QTM_NSTATS];
+    memcpy(g_phase_cycles, ctl_out + 2, sizeof(g_phase_cycles));
     if (ctl_out[1] != ~0ull) {
         const long long row = (long long)ctl_out[1];
         int32_t code = 0;
@@ -617,6 +657,13 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
 }
 
 int qtm_run(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o) { return run_impl(p, a, o, true); }
+
+// phase cycle counters of the last run (all zero unless built with -DQTM_PHASES)
+int qtm_phase_cycles(uint64_t* out16) {
+    if (!out16) return set_error(QTM_ERR_ARGS, "null output");
+    memcpy(out16, g_phase_cycles, sizeof(g_phase_cycles));
+    return QTM_OK;
+}
 
 // FP64 FMA throughput probe (roofline denominator): every thread runs
 // independent DFMA chains; 2 flops per DFMA.

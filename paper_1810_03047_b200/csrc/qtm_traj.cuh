@@ -83,6 +83,7 @@ struct DevProblem {
     // bit k of e_diag_mask set => dense values at e_diag[k * DP + i]
     unsigned e_diag_mask;
     const double2* e_diag;
+    int e_need_gather;      // some observable is not diagonal (needs all of psi)
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
     // per-order constants the reference evaluates inline, tabulated on the
@@ -98,7 +99,8 @@ struct RunParams {
     const long long* script_len;
     long long script_stride;
     double script_fallback;
-    double* values;          // [n_traj][ne][n_pts]
+    double* values;          // [n_traj][ne][n_pts] (written by finalize_records)
+    double* rec_partial;     // [n_traj][n_pts][ne+1][NT/32] per-warp partial sums
     long long* stats;        // [n_traj][NSTATS]
     int* status;             // [n_traj]
     double* err;             // [n_traj][4]: t, h, aux0, aux1   (aux2 = r in err_r)
@@ -110,6 +112,7 @@ struct RunParams {
     double2* zovf;           // [gridDim.x][LROWS-RREG][NT*E]
     unsigned long long* counter;
     unsigned long long* first_fail;  // atomicMin over failing rows
+    unsigned long long* phase_cycles;  // [16] (QTM_PHASES builds only)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -206,6 +209,17 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& phas
     }
 }
 
+
+// Sum over the 32 lanes of a warp; the result is valid in lane 0 (the
+// tree order is fixed, so it is deterministic).
+template <int K>
+__device__ __forceinline__ void warp_sum_lane0(double (&v)[K]) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], m);
+    }
+}
 
 // ------------------------------------------------ Nordsieck history helpers
 // Rows j < RREG are a register array (static indices after unrolling, with
@@ -434,6 +448,20 @@ struct TrajKernel {
 // (every loop over j is fully unrolled), rows >= RREG live in the CTA's
 // overflow scratch.
 #define STAT(which, amount) do { if (tid == 0) s_stats[which] += (amount); } while (0)
+// Phase timing (profiling builds with -DQTM_PHASES): thread 0 attributes
+// clock64() deltas to the phases of the attempt loop.
+#ifdef QTM_PHASES
+#define PH_MARK(k)                                                           \
+    do {                                                                     \
+        if (tid == 0) {                                                      \
+            const long long now__ = clock64();                               \
+            ph_acc[k] += now__ - ph_last;                                    \
+            ph_last = now__;                                                 \
+        }                                                                    \
+    } while (0)
+#else
+#define PH_MARK(k) do { } while (0)
+#endif
 
 template <int NT, int E, int RREG, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
@@ -507,6 +535,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         // hot per-attempt counters live in registers (folded into s_stats at
         // the end of the trajectory); rare events go straight to s_stats
         unsigned c_att = 0, c_q = 0, c_qq = 0, c_it = 0, c_steps = 0;
+#ifdef QTM_PHASES
+        long long ph_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        long long ph_last = clock64();
+#endif
 
         double2 z[RREG][E];  // Nordsieck history rows 0..RREG-1 (registers)
         double w[E];         // error weights 1/(atol + rtol |z0_i|)
@@ -554,16 +586,28 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         var = s_draw;                                                        \
     } while (0)
 
-        // ---- record(gi) of the state in `psi` (trajectory.py:122-130, 206-214)
+        // ---- record(gi) of the state in `psi` (trajectory.py:122-130, 206-214).
+        // The reduction over the state is deferred: every warp stores its
+        // partial <psi|E_k|psi> and <psi|psi> sums, and finalize_records
+        // (qtm_capi.cu) adds the warps in a fixed order and divides.  No
+        // barrier here unless an observable is off-diagonal (then psi is
+        // gathered for the row products).
 #define RECORD(psi, gi_)                                                     \
     do {                                                                     \
-        GATHER(psi, xs__);                                                   \
+        const double2* xs__ = gath;                                          \
+        if (P.e_need_gather) {                                               \
+            GATHER(psi, xg__);                                               \
+            xs__ = xg__;                                                     \
+        }                                                                    \
+        double* const rp__ = R.rec_partial +                                 \
+            ((size_t)row * npts + (gi_)) * (size_t)(P.ne + 1) * (NT / 32) + (tid >> 5); \
         double nrm__ = 0.0;                                                  \
         _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) nrm__ += cabs2(psi[e]); \
-        for (int k0 = 0; k0 < P.ne; k0 += KRED - 1) {                        \
-            double v__[KRED] = {0.0, 0.0, 0.0, nrm__};                       \
-            for (int kk = 0; kk < KRED - 1; ++kk) {                          \
+        for (int k0 = 0; k0 <= P.ne; k0 += KRED) {                           \
+            double v__[KRED];                                                \
+            _Pragma("unroll") for (int kk = 0; kk < KRED; ++kk) {            \
                 const int k = k0 + kk;                                       \
+                double acc__ = 0.0;                                          \
                 if (k < P.ne) {                                              \
                     const bool dg__ = (P.e_diag_mask >> k) & 1u;             \
                     _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) { \
@@ -575,16 +619,17 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         } else {                                             \
                             s = row_dot(P.e[k], II(e), xs__);                \
                         }                                                    \
-                        v__[kk] += psi[e].x * s.x - (-psi[e].y) * s.y;       \
+                        acc__ += psi[e].x * s.x - (-psi[e].y) * s.y;         \
                     }                                                        \
+                } else if (k == P.ne) {                                      \
+                    acc__ = nrm__;                                           \
                 }                                                            \
+                v__[kk] = acc__;                                             \
             }                                                                \
-            block_sum<NT, KRED>(v__, red, rphase);                           \
-            if (v__[KRED - 1] == 0.0) FAIL(kErrZeroVector);                  \
-            if (tid == 0) {                                                  \
-                double* vals__ = R.values + ((size_t)row * P.ne + k0) * npts + (gi_); \
-                for (int kk = 0; kk < KRED - 1; ++kk)                        \
-                    if (k0 + kk < P.ne) vals__[(size_t)kk * npts] = v__[kk] / v__[KRED - 1]; \
+            warp_sum_lane0<KRED>(v__);                                       \
+            if ((tid & 31) == 0) {                                           \
+                _Pragma("unroll") for (int kk = 0; kk < KRED; ++kk)          \
+                    if (k0 + kk <= P.ne) rp__[(size_t)(k0 + kk) * (NT / 32)] = v__[kk]; \
             }                                                                \
         }                                                                    \
     } while (0)
@@ -624,6 +669,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 int nef = 0, ncf = 0;
                 double est = 0.0, nrm2 = 0.0;
                 for (;;) {
+                    PH_MARK(0);  // [0] step-level work since the last mark
                     if (t + h == t) FAIL(kErrStepCollapse);
                     c_att++;
                     c_q += q;
@@ -643,7 +689,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         double2 y0p[E];
 #pragma unroll
                         for (int e = 0; e < E; ++e) y0p[e] = z[0][e];
+                        PH_MARK(1);  // [1] predict
                         GATHER(y0p, xs0);
+                        PH_MARK(2);  // [2] gather z0 + barrier
                     }
                     double2* const ecurp = ebuf + ecur * DP;
                     for (int m = 0; m < 3; ++m) {
@@ -653,6 +701,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         double v[3] = {0.0, 0.0, 0.0};
                         double2 fg[E];
                         GSPMV(cur, fg);
+                        PH_MARK(3);  // [3] SpMV
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
                             if (ACT(e)) {
@@ -668,8 +717,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 ecurp[II(e)] = ei;
                             }
                         }
+                        PH_MARK(4);  // [4] corrector update
                         block_sum<NT, 3>(v, red, rphase);
                         if constexpr (NT == 32) __syncwarp();
+                        PH_MARK(5);  // [5] reduction
                         gbuf ^= 1;
                         del = sqrt(v[0] / (double)d);
                         acc_e = v[1];
@@ -682,7 +733,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         if (del * (c15 < 1.0 ? c15 : 1.0) <= conit) { converged = true; break; }
                         if (m > 0 && del > 2.0 * delp) break;
                         delp = del;
+                        PH_MARK(6);  // [6] convergence control
                     }
+                    PH_MARK(6);
                     if (converged) {
                         est = sqrt(acc_e / (double)d) / P.tau2[q];
                         if (!(est > 1.0)) {
@@ -725,6 +778,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         RESCALE(m1 > 0.1 ? m1 : 0.1);
                     }
                 }
+                PH_MARK(7);  // [7] error test + commit / undo + reject handling
                 // accepted step bookkeeping (ode.py:281-292)
                 t_lo = t;
                 t += h;
@@ -791,6 +845,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     ecur ^= 1;  // e_prev = e
                     has_eprev = true;
                 }
+                PH_MARK(8);  // [8] weights + order/step control
                 // ================= trajectory loop body (trajectory.py:225-246) =======
                 steps_in_segment += 1;
                 if (steps_in_segment > P.max_steps) FAIL(kErrMaxSteps);
@@ -886,15 +941,21 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         continue;
                     }
                 }
+                PH_MARK(9);  // [9] jump test (+ jumps)
                 while (gi < npts && P.times[gi] <= t) {
                     double2 pg[E];
                     HORNER((P.times[gi] - t) / h, pg);
                     RECORD(pg, gi);
                     gi++;
                 }
+                PH_MARK(10);  // [10] grid recording
             }
         }
     traj_done:
+#ifdef QTM_PHASES
+        if (tid == 0)
+            for (int k = 0; k < 12; ++k) atomicAdd(R.phase_cycles + k, (unsigned long long)ph_acc[k]);
+#endif
         if (tid == 0) {
             s_stats[sDraws] = (long long)s_stream.n;
             s_stats[sAttempts] += c_att;
@@ -927,5 +988,6 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 }
 
 #undef STAT
+#undef PH_MARK
 
 }  // namespace qtm

@@ -79,7 +79,7 @@ class QtmRunOut(C.Structure):
 
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
-           "qtm_device_count", "qtm_measure_fp64_peak")
+           "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles")
 
 _lib = None
 
@@ -116,6 +116,9 @@ def lib():
     L.qtm_variant_info.restype = C.c_int
     L.qtm_device_count.argtypes = []
     L.qtm_device_count.restype = C.c_int
+    if hasattr(L, "qtm_phase_cycles"):
+        L.qtm_phase_cycles.argtypes = [C.POINTER(C.c_uint64)]
+        L.qtm_phase_cycles.restype = C.c_int
     L.qtm_measure_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.qtm_measure_fp64_peak.restype = C.c_int
     if L.qtm_abi_version() != ABI_VERSION:
@@ -144,3 +147,13 @@ def fp64_peak_tflops(device: int = 0) -> float:
     if rc != 0:
         raise RuntimeError(f"qtm_measure_fp64_peak failed: {last_error()}")
     return out.value
+
+
+PHASES = ("step-level", "predict", "gather", "spmv", "update", "reduction", "convergence",
+          "error-test/commit", "weights+order-control", "jump-test/jumps", "recording")
+
+
+def phase_cycles():
+    arr = (C.c_uint64 * 16)()
+    lib().qtm_phase_cycles(arr)
+    return {name: int(arr[i]) for i, name in enumerate(PHASES)}
