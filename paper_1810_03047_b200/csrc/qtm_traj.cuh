@@ -22,7 +22,8 @@
 // Differences from the reference are rounding-level only: block reductions
 // are tree sums (the reference sums sequentially), the predicted history is
 // undone in place on a rejected attempt instead of kept in a second copy,
-// and hypot/pow come from CUDA's libdevice (the reference: glibc libm).
+// hypot comes from CUDA's libdevice and the controller's powers from
+// exp2(y*log2(x)) (the reference: glibc hypot/pow).
 #pragma once
 #include <cstdint>
 
@@ -122,6 +123,13 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+
+// est ** (1/(q+1)) etc. in the step-size controller (ode.py:302, 445-453):
+// x > 0 and a small exponent, evaluated as exp2(y * log2(x)); within a few
+// ulp of the correctly rounded power, at a fraction of pow()'s latency.
+__device__ __forceinline__ double ctl_pow(double x, double y) {
+    return x > 0.0 ? exp2(y * log2(x)) : (x == 0.0 ? 0.0 : pow(x, y));
+}
 
 // y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then
 // accumulated (reference _kernels.py:150-154, numba complex_mul).
@@ -773,7 +781,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         has_eprev = false;
                         ialth = q + 1;
                     } else {
-                        const double rr = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
+                        const double rr = 1.0 / (1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
                         const double m1 = 0.9 < rr ? 0.9 : rr;
                         RESCALE(m1 > 0.1 ? m1 : 0.1);
                     }
@@ -791,12 +799,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 ialth -= 1;
                 if (ialth == 0) {
                     // _order_step_control (ode.py:441-466)
-                    const double r_same = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
                     const bool need_d = q > 1;
                     const bool need_u = q < P.max_order && has_eprev;
-                    double r_down = 0.0, r_up = 0.0;
-                    if (need_d || need_u) {
-                        double v[2] = {0.0, 0.0};
+                    double v[2] = {0.0, 0.0};
+                    {
                         const double2* const ecp = ebuf + ecur * DP;
                         const double2* const epp = ebuf + (ecur ^ 1) * DP;
 #pragma unroll
@@ -808,16 +814,17 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 v[1] += cabs2(de) * w[e] * w[e];
                             }
                         }
-                        block_sum<NT, 2>(v, red, rphase);
-                        if (need_d) {
-                            const double est_d = sqrt(v[0] / (double)d) / P.tau1[q];
-                            r_down = 1.0 / (1.3 * pow(est_d, P.rq0[q]) + 1e-6);
-                        }
-                        if (need_u) {
-                            const double est_u = sqrt(v[1] / (double)d) / P.tau3[q];
-                            r_up = 1.0 / (1.4 * pow(est_u, P.rq2[q]) + 1e-6);
-                        }
                     }
+                    block_sum<NT, 2>(v, red, rphase);
+                    // the three candidate ratios are independent: straight-line
+                    // code so their powers overlap (unused ones are discarded)
+                    const double est_d = sqrt(v[0] / (double)d) / P.tau1[q];
+                    const double est_u = sqrt(v[1] / (double)d) / P.tau3[q];
+                    const double r_same = 1.0 / (1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
+                    const double pd = 1.0 / (1.3 * ctl_pow(est_d, P.rq0[q]) + 1e-6);
+                    const double pu = 1.0 / (1.4 * ctl_pow(est_u, P.rq2[q]) + 1e-6);
+                    const double r_down = need_d ? pd : 0.0;
+                    const double r_up = need_u ? pu : 0.0;
                     double best = r_same;
                     if (r_down > best) best = r_down;
                     if (r_up > best) best = r_up;
