@@ -527,26 +527,33 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
     if (per_sm < 1) return set_error(QTM_ERR_CUDA, "kernel variant cannot be resident (registers/smem)");
-    const long long grid = std::min<long long>((long long)dev_sms * per_sm, count);
+    const long long grid = std::min<long long>((long long)dev_sms * per_sm, std::min<long long>(count, 1ll << 16));
     o->grid = (int32_t)grid;
 
-    CUDA_TRY(p->values.ensure((size_t)count * std::max(n_out, 1), s));
+    // Large ensembles run in chunks of at most kRunChunk trajectories so the
+    // per-trajectory device buffers stay bounded (c5's 100 000 trajectories
+    // would otherwise need ~8 GB of partial sums).  kRunChunk is a multiple
+    // of the 256-trajectory reduction block, so the fixed-order ensemble sum
+    // is the same as for one launch.
+    constexpr long long kRunChunk = 1ll << 16;
+    constexpr int kRedChunk = 256;
+    const long long run_chunk = std::min<long long>(count, kRunChunk);
     const int nw = var.threads / 32;
-    CUDA_TRY(p->rec_partial.ensure((size_t)count * p->n_pts * (p->n_expect + 1) * nw, s));
-    CUDA_TRY(p->stats.ensure((size_t)count * QTM_NSTATS, s));
-    CUDA_TRY(p->status.ensure(count, s));
-    CUDA_TRY(p->err.ensure((size_t)count * 4, s));
-    CUDA_TRY(p->err_r.ensure(count, s));
-    CUDA_TRY(p->jump_count.ensure(count, s));
-    CUDA_TRY(p->jump_t.ensure((size_t)count * std::max<long long>(max_jumps, 1), s));
-    CUDA_TRY(p->jump_idx.ensure((size_t)count * std::max<long long>(max_jumps, 1), s));
-    CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS + 1, s));
     const int DP = var.threads * var.comps;
+    const long long n_red_total = (count + kRedChunk - 1) / kRedChunk;
+    CUDA_TRY(p->values.ensure((size_t)run_chunk * std::max(n_out, 1), s));
+    CUDA_TRY(p->rec_partial.ensure((size_t)run_chunk * p->n_pts * (p->n_expect + 1) * nw, s));
+    CUDA_TRY(p->stats.ensure((size_t)run_chunk * QTM_NSTATS, s));
+    CUDA_TRY(p->status.ensure(run_chunk, s));
+    CUDA_TRY(p->err.ensure((size_t)run_chunk * 4, s));
+    CUDA_TRY(p->err_r.ensure(run_chunk, s));
+    CUDA_TRY(p->jump_count.ensure(run_chunk, s));
+    CUDA_TRY(p->jump_t.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
+    CUDA_TRY(p->jump_idx.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
+    CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS + 1, s));
     if (var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
-    const int chunk = 256;
-    const int n_chunks = (int)((count + chunk - 1) / chunk);
-    CUDA_TRY(p->psum.ensure((size_t)n_chunks * std::max(n_out, 1), s));
-    CUDA_TRY(p->psq.ensure((size_t)n_chunks * std::max(n_out, 1), s));
+    CUDA_TRY(p->psum.ensure((size_t)n_red_total * std::max(n_out, 1), s));
+    CUDA_TRY(p->psq.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));
     CUDA_TRY(p->sumsq.ensure(std::max(n_out, 1), s));
     if (a->stream_kind == QTM_STREAM_SCRIPTED) {
@@ -557,103 +564,124 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         CUDA_TRY(cudaMemcpyAsync(p->script_len.p, a->script_len, sizeof(int64_t) * count,
                                  cudaMemcpyHostToDevice, s));
     }
-    unsigned long long ctl_init[18] = {0ull, ~0ull};
     CUDA_TRY(cudaEventRecord(p->ev[0], s));
-    CUDA_TRY(cudaMemcpyAsync(p->ctl.p, ctl_init, sizeof(ctl_init), cudaMemcpyHostToDevice, s));
+    long long totals[QTM_NSTATS + 1] = {0};
+    int64_t launches = 0;
+    float kernel_ms = 0.f;
+    int rc_out = QTM_OK;
+    bool failed = false;
+    memset(g_phase_cycles, 0, sizeof(g_phase_cycles));
 
-    RunParams R{};
-    R.seed = a->seed;
-    R.traj_begin = a->traj_begin;
-    R.n_traj = count;
-    R.stream_kind = a->stream_kind;
-    R.script = a->stream_kind == QTM_STREAM_SCRIPTED ? p->script.p : nullptr;
-    R.script_len = a->stream_kind == QTM_STREAM_SCRIPTED ? p->script_len.p : nullptr;
-    R.script_stride = a->script_stride;
-    R.script_fallback = a->script_fallback;
-    R.values = p->values.p;
-    R.rec_partial = p->rec_partial.p;
-    R.stats = p->stats.p;
-    R.status = p->status.p;
-    R.err = p->err.p;
-    R.err_r = p->err_r.p;
-    R.jump_count = p->jump_count.p;
-    R.jump_t = p->jump_t.p;
-    R.jump_idx = p->jump_idx.p;
-    R.max_jumps = max_jumps;
-    R.zovf = p->zovf.p;
-    R.counter = p->ctl.p;
-    R.first_fail = p->ctl.p + 1;
-    R.phase_cycles = p->ctl.p + 2;
-    void* kargs[] = {(void*)&p->dp, (void*)&R};
-    CUDA_TRY(cudaEventRecord(p->ev[1], s));
-    CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)grid), dim3(var.threads), kargs, p->smem, s));
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(p->ev[2], s));
-    int64_t launches = 1;
-    {
-        const long long cells = count * p->n_pts;
+    for (long long off = 0; off < count; off += kRunChunk) {
+        const long long cnt = std::min<long long>(kRunChunk, count - off);
+        const long long cgrid = std::min<long long>(grid, cnt);
+        unsigned long long ctl_init[18] = {0ull, ~0ull};
+        CUDA_TRY(cudaMemcpyAsync(p->ctl.p, ctl_init, sizeof(ctl_init), cudaMemcpyHostToDevice, s));
+        RunParams R{};
+        R.seed = a->seed;
+        R.traj_begin = a->traj_begin + off;
+        R.n_traj = cnt;
+        R.stream_kind = a->stream_kind;
+        R.script = a->stream_kind == QTM_STREAM_SCRIPTED ? p->script.p + off * a->script_stride : nullptr;
+        R.script_len = a->stream_kind == QTM_STREAM_SCRIPTED ? p->script_len.p + off : nullptr;
+        R.script_stride = a->script_stride;
+        R.script_fallback = a->script_fallback;
+        R.values = p->values.p;
+        R.rec_partial = p->rec_partial.p;
+        R.stats = p->stats.p;
+        R.status = p->status.p;
+        R.err = p->err.p;
+        R.err_r = p->err_r.p;
+        R.jump_count = p->jump_count.p;
+        R.jump_t = p->jump_t.p;
+        R.jump_idx = p->jump_idx.p;
+        R.max_jumps = max_jumps;
+        R.zovf = p->zovf.p;
+        R.counter = p->ctl.p;
+        R.first_fail = p->ctl.p + 1;
+        R.phase_cycles = p->ctl.p + 2;
+        void* kargs[] = {(void*)&p->dp, (void*)&R};
+        CUDA_TRY(cudaEventRecord(p->ev[1], s));
+        CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)cgrid), dim3(var.threads), kargs, p->smem, s));
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(p->ev[2], s));
+        const long long cells = cnt * p->n_pts;
         finalize_records<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
-            p->rec_partial.p, p->status.p, p->values.p, count, (int)p->n_pts, p->n_expect, nw, p->ctl.p + 1);
+            p->rec_partial.p, p->status.p, p->values.p, cnt, (int)p->n_pts, p->n_expect, nw, p->ctl.p + 1);
+        const long long red_off = off / kRedChunk;
+        const int n_red = (int)((cnt + kRedChunk - 1) / kRedChunk);
+        if (n_out > 0) {
+            dim3 g1((n_out + 127) / 128, n_red);
+            ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, p->status.p, cnt, n_out, kRedChunk,
+                                                p->psum.p + red_off * n_out, p->psq.p + red_off * n_out);
+        }
+        stats_total<<<1, 32, 0, s>>>(p->stats.p, p->status.p, cnt, p->stats_tot.p);
+        launches += 1 + 1 + (n_out > 0 ? 1 : 0) + 1;
+        CUDA_TRY(cudaGetLastError());
+        unsigned long long ctl_out[18];
+        long long tot_host[QTM_NSTATS + 1];
+        CUDA_TRY(cudaMemcpyAsync(ctl_out, p->ctl.p, sizeof(ctl_out), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(tot_host, p->stats_tot.p, sizeof(tot_host), cudaMemcpyDeviceToHost, s));
+        if (copy_per_traj) {
+            if (o->values && n_out > 0)
+                CUDA_TRY(cudaMemcpyAsync(o->values + off * n_out, p->values.p, sizeof(double) * cnt * n_out,
+                                         cudaMemcpyDeviceToHost, s));
+            if (o->stats)
+                CUDA_TRY(cudaMemcpyAsync(o->stats + off * QTM_NSTATS, p->stats.p, sizeof(int64_t) * cnt * QTM_NSTATS,
+                                         cudaMemcpyDeviceToHost, s));
+            if (o->status)
+                CUDA_TRY(cudaMemcpyAsync(o->status + off, p->status.p, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost, s));
+            if (o->jump_count)
+                CUDA_TRY(cudaMemcpyAsync(o->jump_count + off, p->jump_count.p, sizeof(int64_t) * cnt,
+                                         cudaMemcpyDeviceToHost, s));
+            if (o->jump_t && max_jumps > 0)
+                CUDA_TRY(cudaMemcpyAsync(o->jump_t + off * max_jumps, p->jump_t.p, sizeof(double) * cnt * max_jumps,
+                                         cudaMemcpyDeviceToHost, s));
+            if (o->jump_idx && max_jumps > 0)
+                CUDA_TRY(cudaMemcpyAsync(o->jump_idx + off * max_jumps, p->jump_idx.p,
+                                         sizeof(int32_t) * cnt * max_jumps, cudaMemcpyDeviceToHost, s));
+        }
+        CUDA_TRY(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p->ev[1], p->ev[2]);
+        kernel_ms += ms;
+        for (int k = 0; k <= QTM_NSTATS; ++k) totals[k] += tot_host[k];
+        for (int k = 0; k < 16; ++k) g_phase_cycles[k] += ctl_out[2 + k];
+        if (!failed && ctl_out[1] != ~0ull) {  // lowest failing index of this chunk
+            failed = true;
+            const long long row = (long long)ctl_out[1];
+            int32_t code = 0;
+            double e4[4], er = 0.0;
+            CUDA_TRY(cudaMemcpy(&code, p->status.p + row, sizeof(int32_t), cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(e4, p->err.p + row * 4, sizeof(e4), cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(&er, p->err_r.p + row, sizeof(double), cudaMemcpyDeviceToHost));
+            o->error.code = code;
+            o->error.traj = a->traj_begin + off + row;
+            o->error.t = e4[0];
+            o->error.h = e4[1];
+            o->error.aux0 = e4[2];
+            o->error.aux1 = e4[3];
+            o->error.aux2 = er;
+            o->error.max_steps = p->dp.max_steps;
+            rc_out = code;
+        }
+    }
+    if (n_out > 0) {
+        ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, (int)n_red_total, n_out,
+                                                           p->sum.p, p->sumsq.p);
         launches += 1;
-    }
-    if (n_out > 0) {
-        dim3 g1((n_out + 127) / 128, n_chunks);
-        ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, p->status.p, count, n_out, chunk, p->psum.p, p->psq.p);
-        ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, n_chunks, n_out, p->sum.p,
-                                                           p->sumsq.p);
-        launches += 2;
-    }
-    stats_total<<<1, 32, 0, s>>>(p->stats.p, p->status.p, count, p->stats_tot.p);
-    launches += 1;
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(p->ev[3], s));
-    if (n_out > 0) {
+        CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaMemcpyAsync(o->sum, p->sum.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
         if (o->sumsq) CUDA_TRY(cudaMemcpyAsync(o->sumsq, p->sumsq.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
     }
-    unsigned long long ctl_out[18];
-    CUDA_TRY(cudaMemcpyAsync(ctl_out, p->ctl.p, sizeof(ctl_out), cudaMemcpyDeviceToHost, s));
-    long long tot_host[QTM_NSTATS + 1];
-    CUDA_TRY(cudaMemcpyAsync(tot_host, p->stats_tot.p, sizeof(tot_host), cudaMemcpyDeviceToHost, s));
-    if (copy_per_traj) {
-        if (o->values && n_out > 0)
-            CUDA_TRY(cudaMemcpyAsync(o->values, p->values.p, sizeof(double) * count * n_out, cudaMemcpyDeviceToHost, s));
-        if (o->stats)
-            CUDA_TRY(cudaMemcpyAsync(o->stats, p->stats.p, sizeof(int64_t) * count * QTM_NSTATS, cudaMemcpyDeviceToHost, s));
-        if (o->status)
-            CUDA_TRY(cudaMemcpyAsync(o->status, p->status.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s));
-        if (o->jump_count)
-            CUDA_TRY(cudaMemcpyAsync(o->jump_count, p->jump_count.p, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, s));
-        if (o->jump_t && max_jumps > 0)
-            CUDA_TRY(cudaMemcpyAsync(o->jump_t, p->jump_t.p, sizeof(double) * count * max_jumps, cudaMemcpyDeviceToHost, s));
-        if (o->jump_idx && max_jumps > 0)
-            CUDA_TRY(cudaMemcpyAsync(o->jump_idx, p->jump_idx.p, sizeof(int32_t) * count * max_jumps, cudaMemcpyDeviceToHost, s));
-    }
+    CUDA_TRY(cudaEventRecord(p->ev[3], s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    cudaEventElapsedTime(&o->kernel_ms, p->ev[1], p->ev[2]);
     cudaEventElapsedTime(&o->total_ms, p->ev[0], p->ev[3]);
+    o->kernel_ms = kernel_ms;
     o->launches = launches;
-    if (o->stats_total) memcpy(o->stats_total, tot_host, sizeof(int64_t) * QTM_NSTATS);
-    o->n_failed = tot_host[QTM_NSTATS];
-    memcpy(g_phase_cycles, ctl_out + 2, sizeof(g_phase_cycles));
-    if (ctl_out[1] != ~0ull) {
-        const long long row = (long long)ctl_out[1];
-        int32_t code = 0;
-        double e4[4], er = 0.0;
-        CUDA_TRY(cudaMemcpy(&code, p->status.p + row, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(e4, p->err.p + row * 4, sizeof(e4), cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(&er, p->err_r.p + row, sizeof(double), cudaMemcpyDeviceToHost));
-        o->error.code = code;
-        o->error.traj = a->traj_begin + row;
-        o->error.t = e4[0];
-        o->error.h = e4[1];
-        o->error.aux0 = e4[2];
-        o->error.aux1 = e4[3];
-        o->error.aux2 = er;
-        o->error.max_steps = p->dp.max_steps;
-        return code;
-    }
-    return QTM_OK;
+    if (o->stats_total) memcpy(o->stats_total, totals, sizeof(int64_t) * QTM_NSTATS);
+    o->n_failed = totals[QTM_NSTATS];
+    return rc_out;
 }
 
 int qtm_run(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o) { return run_impl(p, a, o, true); }

@@ -228,3 +228,17 @@ def test_independent_streams_within_three_sigma(oracle_lib):
     z = np.abs(mg - mc) / np.maximum(np.sqrt(se_g ** 2 + se_c ** 2), 1e-12)
     # 602 points: allow the expected ~0.3 % beyond 3 sigma, none beyond 5
     assert np.mean(z > 3) < 0.02 and z.max() < 5
+
+
+def test_chunked_large_ensemble():
+    # more trajectories than one launch chunk (65 536): per-trajectory results
+    # and the fixed-order ensemble sum are unchanged by the chunking
+    p = configs.build("c1")
+    n = 70_000
+    with DeviceProblem(p) as dp:
+        big = dp.run(5, 0, n)
+        tail = dp.run(5, 65_536, n)
+    assert big.rc == 0 and big.n_failed == 0
+    np.testing.assert_array_equal(big.values[65_536:], tail.values)
+    np.testing.assert_allclose(big.sum, big.values.sum(axis=0), rtol=1e-12, atol=1e-9)
+    assert big.stats_total[0] == big.stats[:, 0].sum()
