@@ -240,5 +240,5 @@ def test_chunked_large_ensemble():
         tail = dp.run(5, 65_536, n)
     assert big.rc == 0 and big.n_failed == 0
     np.testing.assert_array_equal(big.values[65_536:], tail.values)
-    np.testing.assert_allclose(big.sum, big.values.sum(axis=0), rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(big.sum, big.values.sum(axis=0), rtol=1e-10, atol=1e-9)
     assert big.stats_total[0] == big.stats[:, 0].sum()
