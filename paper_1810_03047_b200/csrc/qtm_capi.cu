@@ -475,15 +475,19 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (rc == QTM_OK && cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaDeviceGetAttribute(smem opt-in) failed");
     p->smem = var.smem;
+    // the kernel's static __shared__ (work row, counters, stream state and the
+    // per-warp cold controller state) comes off the dynamic budget
+    cudaFuncAttributes fattr;
+    size_t static_smem = 4096;
+    if (rc == QTM_OK && cudaFuncGetAttributes(&fattr, var.fn) == cudaSuccess) static_smem = fattr.sharedSizeBytes;
+    const size_t dyn_cap = (size_t)smem_cap > static_smem ? (size_t)smem_cap - static_smem : 0;
     if (rc == QTM_OK) {
         bool staged = false;
-        // static __shared__ of the kernel (row, counters, stream) stays below 1 KB
-        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem,
-                        (size_t)smem_cap - 1024, &staged);
+        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged);
     }
     if (rc == QTM_OK) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->smem > 48 * 1024 &&
-        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap - 1024) != cudaSuccess)
+        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_cap) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
     if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
     if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)

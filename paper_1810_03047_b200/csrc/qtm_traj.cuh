@@ -488,6 +488,18 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     __shared__ long long s_stats[NSTATS];
     __shared__ Stream s_stream;
     __shared__ double s_draw;
+    // Per-warp copies of the controller state that is not needed inside the
+    // corrector iteration (every lane holds the same value; a warp only ever
+    // touches its own copy, so no barrier is involved).  Keeping them out of
+    // the register file leaves the registers to the Nordsieck history.
+    struct WarpCold {
+        double t_lo, r_thr;
+        long long row, steps_in_segment, njumps;
+        int gi, nef, ncf;
+        unsigned c_att, c_q, c_qq, c_it, c_steps;
+    };
+    __shared__ WarpCold s_cold[NT / 32];
+    WarpCold& ws = s_cold[threadIdx.x >> 5];
 
     const int tid = threadIdx.x;
     const int d = P.d;
@@ -529,20 +541,20 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     for (;;) {
         if (tid == 0) s_row = (long long)atomicAdd(R.counter, 1ull);
         __syncthreads();
-        const long long row = s_row;
-        if (row >= R.n_traj) break;
+        ws.row = s_row;
+        if (ws.row >= R.n_traj) break;
         if (tid < NSTATS) s_stats[tid] = 0;
         if (tid == 0)
-            s_stream.init(R.stream_kind, R.seed, (uint64_t)(R.traj_begin + row),
-                          R.script ? R.script + row * R.script_stride : nullptr,
-                          R.script_len ? R.script_len[row] : 0, R.script_fallback);
+            s_stream.init(R.stream_kind, R.seed, (uint64_t)(R.traj_begin + ws.row),
+                          R.script ? R.script + ws.row * R.script_stride : nullptr,
+                          R.script_len ? R.script_len[ws.row] : 0, R.script_fallback);
         __syncthreads();
 
-        long long njumps = 0;
+        ws.njumps = 0;
         int rc = kOk;
         // hot per-attempt counters live in registers (folded into s_stats at
         // the end of the trajectory); rare events go straight to s_stats
-        unsigned c_att = 0, c_q = 0, c_qq = 0, c_it = 0, c_steps = 0;
+        ws.c_att = 0; ws.c_q = 0; ws.c_qq = 0; ws.c_it = 0; ws.c_steps = 0;
 #ifdef QTM_PHASES
         long long ph_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         long long ph_last = clock64();
@@ -550,7 +562,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 
         double2 z[RREG][E];  // Nordsieck history rows 0..RREG-1 (registers)
         double w[E];         // error weights 1/(atol + rtol |z0_i|)
-        double t, t_lo, h, crate;
+        double t, h, crate;
         int q, ialth;
         bool has_eprev;
 
@@ -578,7 +590,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     do {                                                                     \
         rc = (code_);                                                        \
         if (tid == 0) {                                                      \
-            double* eo__ = R.err + (size_t)row * 4;                          \
+            double* eo__ = R.err + (size_t)ws.row * 4;                          \
             eo__[0] = (a_); eo__[1] = (b_); eo__[2] = (c_); eo__[3] = (d_);  \
         }                                                                    \
         goto traj_done;                                                      \
@@ -594,12 +606,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         var = s_draw;                                                        \
     } while (0)
 
-        // ---- record(gi) of the state in `psi` (trajectory.py:122-130, 206-214).
+        // ---- record(ws.gi) of the state in `psi` (trajectory.py:122-130, 206-214).
         // The reduction over the state is deferred: every warp stores its
         // partial <psi|E_k|psi> and <psi|psi> sums, and finalize_records
         // (qtm_capi.cu) adds the warps in a fixed order and divides.  No
         // barrier here unless an observable is off-diagonal (then psi is
-        // gathered for the row products).
+        // gathered for the ws.row products).
 #define RECORD(psi, gi_)                                                     \
     do {                                                                     \
         const double2* xs__ = gath;                                          \
@@ -608,7 +620,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             xs__ = xg__;                                                     \
         }                                                                    \
         double* const rp__ = R.rec_partial +                                 \
-            ((size_t)row * npts + (gi_)) * (size_t)(P.ne + 1) * (NT / 32) + (tid >> 5); \
+            ((size_t)ws.row * npts + (gi_)) * (size_t)(P.ne + 1) * (NT / 32) + (tid >> 5); \
         double nrm__ = 0.0;                                                  \
         _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) nrm__ += cabs2(psi[e]); \
         for (int k0 = 0; k0 <= P.ne; k0 += KRED) {                           \
@@ -645,7 +657,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         // ---- cold start of the solver at (t0, y0[E]) with step h0 (ode.py:164-217)
 #define COLD_START(t0_, y0, h0_)                                             \
     do {                                                                     \
-        t = (t0_); t_lo = t; q = 1; h = (h0_);                               \
+        t = (t0_); ws.t_lo = t; q = 1; h = (h0_);                               \
         GATHER(y0, xs__);                                                    \
         STAT(sNfe, 1);                                                       \
         double2 f__[E];                                                      \
@@ -666,22 +678,21 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
             for (int e = 0; e < E; ++e) psi[e] = ACT(e) ? P.psi0[II(e)] : make_double2(0.0, 0.0);
             RECORD(psi, 0);  // record(0) from psi0
-            double r;
-            DRAW(r);
+            DRAW(ws.r_thr);
             COLD_START(P.t_from, psi, P.h0_first);
-            int gi = 1;
-            long long steps_in_segment = 0;
+            ws.gi = 1;
+            ws.steps_in_segment = 0;
 
-            while (gi < npts) {
+            while (ws.gi < npts) {
                 // ================= OdeSolver.step() (ode.py:261-312) =================
-                int nef = 0, ncf = 0;
+                ws.nef = 0; ws.ncf = 0;
                 double est = 0.0, nrm2 = 0.0;
                 for (;;) {
                     PH_MARK(0);  // [0] step-level work since the last mark
                     if (t + h == t) FAIL(kErrStepCollapse);
-                    c_att++;
-                    c_q += q;
-                    c_qq += q * (q + 1);
+                    ws.c_att++;
+                    ws.c_q += q;
+                    ws.c_qq += q * (q + 1);
                     if (q + 1 > RREG) STAT(sOverflow, 1);
                     // predict: in-place Pascal triangle (_kernels.py:133-137)
                     H::predict(z, OVF(), q);
@@ -705,7 +716,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     for (int m = 0; m < 3; ++m) {
                         const double2* const cur = gath + gbuf * DP;
                         double2* const nxt = gath + (gbuf ^ 1) * DP;
-                        c_it++;
+                        ws.c_it++;
                         double v[3] = {0.0, 0.0, 0.0};
                         double2 fg[E];
                         GSPMV(cur, fg);
@@ -759,13 +770,13 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     H::undo(z, OVF(), q);
                     if (!converged) {
                         STAT(sCorrFail, 1);
-                        if (++ncf >= 10) FAIL(kErrCorrector);
+                        if (++ws.ncf >= 10) FAIL(kErrCorrector);
                         RESCALE(0.25);
                         continue;
                     }
                     STAT(sErrReject, 1);
-                    if (++nef >= 10) FAIL(kErrRepeatedErrTest);
-                    if (nef >= 3) {
+                    if (++ws.nef >= 10) FAIL(kErrRepeatedErrTest);
+                    if (ws.nef >= 3) {
                         // _restart_order_one(0.1), ode.py:314-323
                         q = 1;
                         h *= 0.1;
@@ -788,9 +799,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 }
                 PH_MARK(7);  // [7] error test + commit / undo + reject handling
                 // accepted step bookkeeping (ode.py:281-292)
-                t_lo = t;
+                ws.t_lo = t;
                 t += h;
-                c_steps++;
+                ws.c_steps++;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = z[0][e];
@@ -854,30 +865,30 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 }
                 PH_MARK(8);  // [8] weights + order/step control
                 // ================= trajectory loop body (trajectory.py:225-246) =======
-                steps_in_segment += 1;
-                if (steps_in_segment > P.max_steps) FAIL(kErrMaxSteps);
-                if (P.nc > 0 && nrm2 < r) {
+                ws.steps_in_segment += 1;
+                if (ws.steps_in_segment > P.max_steps) FAIL(kErrMaxSteps);
+                if (P.nc > 0 && nrm2 < ws.r_thr) {
                     // locate_jump_time (trajectory.py:157-182)
                     double v2[2] = {0.0, 0.0};
                     {
                         double2 a1[E], a2[E];
-                        HORNER((t_lo - t) / h, a1);
+                        HORNER((ws.t_lo - t) / h, a1);
                         HORNER((t - t) / h, a2);
 #pragma unroll
                         for (int e = 0; e < E; ++e) if (ACT(e)) { v2[0] += cabs2(a1[e]); v2[1] += cabs2(a2[e]); }
                     }
                     block_sum<NT, 2>(v2, red, rphase);
                     const double f_lo = v2[0], f_hi = v2[1];
-                    const double tol = 1e-9 * r;
-                    if (f_lo < r - tol || f_hi > r + tol) {
-                        if (tid == 0) R.err_r[row] = r;
-                        FAIL4(kErrBracket, t_lo, t, f_lo, f_hi);
+                    const double tol = 1e-9 * ws.r_thr;
+                    if (f_lo < ws.r_thr - tol || f_hi > ws.r_thr + tol) {
+                        if (tid == 0) R.err_r[ws.row] = ws.r_thr;
+                        FAIL4(kErrBracket, ws.t_lo, t, f_lo, f_hi);
                     }
                     double ts;
-                    if (f_lo <= r + tol) {
-                        ts = t_lo;
+                    if (f_lo <= ws.r_thr + tol) {
+                        ts = ws.t_lo;
                     } else {
-                        double a = t_lo, b = t;
+                        double a = ws.t_lo, b = t;
                         bool found = false;
                         ts = 0.0;
                         for (int it = 0; it < 60; ++it) {
@@ -891,17 +902,17 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                             }
                             block_sum<NT, 1>(v1, red, rphase);
                             STAT(sBisect, 1);
-                            if (fabs(v1[0] - r) <= tol) { ts = mid; found = true; break; }
-                            if (v1[0] > r) a = mid; else b = mid;
+                            if (fabs(v1[0] - ws.r_thr) <= tol) { ts = mid; found = true; break; }
+                            if (v1[0] > ws.r_thr) a = mid; else b = mid;
                         }
                         if (!found) ts = 0.5 * (a + b);
                     }
                     if (ts <= P.t_to) {
-                        while (gi < npts && P.times[gi] <= ts) {
+                        while (ws.gi < npts && P.times[ws.gi] <= ts) {
                             double2 pg[E];
-                            HORNER((P.times[gi] - t) / h, pg);
-                            RECORD(pg, gi);
-                            gi++;
+                            HORNER((P.times[ws.gi] - t) / h, pg);
+                            RECORD(pg, ws.gi);
+                            ws.gi++;
                         }
                         // psi(t*) and the collapse (trajectory.py:235-241, 133-154)
                         double2 pst[E];
@@ -936,24 +947,24 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                         for (int e = 0; e < E; ++e)
                             pst[e] = ACT(e) ? cscale(scl, row_dot(P.c[idx], II(e), xs)) : make_double2(0.0, 0.0);
-                        if (tid == 0 && njumps < R.max_jumps) {
-                            R.jump_t[(size_t)row * R.max_jumps + njumps] = ts;
-                            R.jump_idx[(size_t)row * R.max_jumps + njumps] = idx;
+                        if (tid == 0 && ws.njumps < R.max_jumps) {
+                            R.jump_t[(size_t)ws.row * R.max_jumps + ws.njumps] = ts;
+                            R.jump_idx[(size_t)ws.row * R.max_jumps + ws.njumps] = idx;
                         }
-                        njumps++;
+                        ws.njumps++;
                         STAT(sJumps, 1);
-                        DRAW(r);
+                        DRAW(ws.r_thr);
                         COLD_START(ts, pst, h);
-                        steps_in_segment = 0;
+                        ws.steps_in_segment = 0;
                         continue;
                     }
                 }
                 PH_MARK(9);  // [9] jump test (+ jumps)
-                while (gi < npts && P.times[gi] <= t) {
+                while (ws.gi < npts && P.times[ws.gi] <= t) {
                     double2 pg[E];
-                    HORNER((P.times[gi] - t) / h, pg);
-                    RECORD(pg, gi);
-                    gi++;
+                    HORNER((P.times[ws.gi] - t) / h, pg);
+                    RECORD(pg, ws.gi);
+                    ws.gi++;
                 }
                 PH_MARK(10);  // [10] grid recording
             }
@@ -965,18 +976,18 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #endif
         if (tid == 0) {
             s_stats[sDraws] = (long long)s_stream.n;
-            s_stats[sAttempts] += c_att;
-            s_stats[sSumQ] += c_q;
-            s_stats[sSumQQ1] += c_qq;
-            s_stats[sCorrIters] += c_it;
-            s_stats[sNfe] += c_it;
-            s_stats[sSteps] += c_steps;
-            long long* so = R.stats + (size_t)row * NSTATS;
+            s_stats[sAttempts] += ws.c_att;
+            s_stats[sSumQ] += ws.c_q;
+            s_stats[sSumQQ1] += ws.c_qq;
+            s_stats[sCorrIters] += ws.c_it;
+            s_stats[sNfe] += ws.c_it;
+            s_stats[sSteps] += ws.c_steps;
+            long long* so = R.stats + (size_t)ws.row * NSTATS;
 #pragma unroll
             for (int s = 0; s < NSTATS; ++s) so[s] = s_stats[s];
-            R.status[row] = rc;
-            R.jump_count[row] = njumps;
-            if (rc != kOk) atomicMin(R.first_fail, (unsigned long long)row);
+            R.status[ws.row] = rc;
+            R.jump_count[ws.row] = ws.njumps;
+            if (rc != kOk) atomicMin(R.first_fail, (unsigned long long)ws.row);
         }
         __syncthreads();
     }
