@@ -177,6 +177,26 @@ def cpu_reference(packed, sample: int, steps: int, warmup: int, threads: int):
 CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1}
 
 
+def profiled_traffic(config: str):
+    """DRAM bytes per launch of the trajectory kernel from the committed ncu
+    --set full capture of this config (profiles/r01_<config>_traj_kernel_raw_selected.csv),
+    or None when there is none."""
+    path = os.path.join(REPO, "profiles", f"r01_{config}_traj_kernel_raw_selected.csv")
+    if not os.path.exists(path):
+        return None
+    vals = {}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    with open(path) as f:
+        for line in f:
+            parts = line.strip().split(",")
+            if len(parts) == 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                vals[parts[0]] = float(parts[2]) * scale.get(parts[1], 1.0)
+    if len(vals) != 2:
+        return None
+    return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+            "source": os.path.relpath(path, REPO)}
+
+
 def _sum_over_ranks(dist, torch, local, x, world):
     if world == 1:
         return x
@@ -378,7 +398,8 @@ def main(argv=None):
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None,
+                         "traffic": (profiled_traffic(args.config) or {}).get("bytes"),
+                         "traffic_source": (profiled_traffic(args.config) or {}).get("source"),
                          "kernel": "traj_kernel (persistent; state in registers/smem)",
                          "peak_source": "measured DFMA throughput on this GPU "
                                         "(qtm_measure_fp64_peak, 2 flops/DFMA)",
