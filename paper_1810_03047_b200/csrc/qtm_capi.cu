@@ -454,7 +454,11 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         P.rq1[q] = 1.0 / (q + 1);
         P.rq0[q] = q ? 1.0 / q : 0.0;
         P.rq2[q] = 1.0 / (q + 2);
+        P.inv_tau1[q] = P.tau1[q] != 0.0 ? 1.0 / P.tau1[q] : 0.0;
+        P.inv_tau2[q] = P.tau2[q] != 0.0 ? 1.0 / P.tau2[q] : 0.0;
+        P.inv_tau3[q] = P.tau3[q] != 0.0 ? 1.0 / P.tau3[q] : 0.0;
     }
+    P.inv_d = 1.0 / (double)d->dim;
     rc = upload_csr(p, d->generator, d->dim, &P.g, "generator");
     for (int c = 0; rc == QTM_OK && c < d->n_collapse; ++c) rc = upload_csr(p, d->collapse[c], d->dim, &P.c[c], "collapse");
     for (int k = 0; rc == QTM_OK && k < d->n_expect; ++k) rc = upload_csr(p, d->expect[k], d->dim, &P.e[k], "expect");

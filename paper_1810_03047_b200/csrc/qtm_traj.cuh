@@ -22,8 +22,10 @@
 // Differences from the reference are rounding-level only: block reductions
 // are tree sums (the reference sums sequentially), the predicted history is
 // undone in place on a rejected attempt instead of kept in a second copy,
-// hypot comes from CUDA's libdevice and the controller's powers from
-// exp2(y*log2(x)) (the reference: glibc hypot/pow).
+// WRMS norms multiply by host-computed reciprocals of d and tau instead of
+// dividing (FP64 division sits on the per-attempt critical path),
+// hypot comes from CUDA's libdevice and the controller's fractional
+// powers from a Newton-refined root (the reference: glibc hypot/pow).
 #pragma once
 #include <cstdint>
 
@@ -90,6 +92,10 @@ struct DevProblem {
     // per-order constants the reference evaluates inline, tabulated on the
     // host with the same IEEE operations: 0.5/(q+2), 1/(q+1), 1/q, 1/(q+2)
     double conit[LROWS], rq1[LROWS], rq0[LROWS], rq2[LROWS];
+    // reciprocals for the WRMS norms: sqrt(acc / d) / tau becomes
+    // sqrt(acc * inv_d) * inv_tau (last-bit differences only)
+    double inv_d;
+    double inv_tau1[LROWS], inv_tau2[LROWS], inv_tau3[LROWS];
 };
 
 struct RunParams {
@@ -666,7 +672,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             z[0][e] = (y0)[e];                                               \
             z[1][e] = cscale(h, f__[e]);                                     \
             _Pragma("unroll") for (int j = 2; j < RREG; ++j) z[j][e] = make_double2(0.0, 0.0); \
-            w[e] = ACT(e) ? 1.0 / (P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
+            w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
         }                                                                    \
         crate = 0.7; ialth = 2; has_eprev = false;                           \
     } while (0)
@@ -741,7 +747,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         if constexpr (NT == 32) __syncwarp();
                         PH_MARK(5);  // [5] reduction
                         gbuf ^= 1;
-                        del = sqrt(v[0] / (double)d);
+                        del = sqrt(v[0] * P.inv_d);
                         acc_e = v[1];
                         nrm2 = v[2];
                         if (m > 0) {
@@ -756,7 +762,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     }
                     PH_MARK(6);
                     if (converged) {
-                        est = sqrt(acc_e / (double)d) / P.tau2[q];
+                        est = sqrt(acc_e * P.inv_d) * P.inv_tau2[q];
                         if (!(est > 1.0)) {
                             // commit zp[j] += l_j e (_kernels.py:187-191)
                             double2 evr[E];
@@ -792,7 +798,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         has_eprev = false;
                         ialth = q + 1;
                     } else {
-                        const double rr = 1.0 / (1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
+                        const double rr = __drcp_rn(1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
                         const double m1 = 0.9 < rr ? 0.9 : rr;
                         RESCALE(m1 > 0.1 ? m1 : 0.1);
                     }
@@ -805,7 +811,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = z[0][e];
-                    w[e] = ACT(e) ? 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
+                    w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
                 }
                 ialth -= 1;
                 if (ialth == 0) {
@@ -829,11 +835,11 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     block_sum<NT, 2>(v, red, rphase);
                     // the three candidate ratios are independent: straight-line
                     // code so their powers overlap (unused ones are discarded)
-                    const double est_d = sqrt(v[0] / (double)d) / P.tau1[q];
-                    const double est_u = sqrt(v[1] / (double)d) / P.tau3[q];
-                    const double r_same = 1.0 / (1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
-                    const double pd = 1.0 / (1.3 * ctl_pow(est_d, P.rq0[q]) + 1e-6);
-                    const double pu = 1.0 / (1.4 * ctl_pow(est_u, P.rq2[q]) + 1e-6);
+                    const double est_d = sqrt(v[0] * P.inv_d) * P.inv_tau1[q];
+                    const double est_u = sqrt(v[1] * P.inv_d) * P.inv_tau3[q];
+                    const double r_same = __drcp_rn(1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
+                    const double pd = __drcp_rn(1.3 * ctl_pow(est_d, P.rq0[q]) + 1e-6);
+                    const double pu = __drcp_rn(1.4 * ctl_pow(est_u, P.rq2[q]) + 1e-6);
                     const double r_down = need_d ? pd : 0.0;
                     const double r_up = need_u ? pu : 0.0;
                     double best = r_same;
