@@ -813,6 +813,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     const double2 z0 = z[0][e];
                     w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
                 }
+                PH_MARK(11);  // [11] accepted-step bookkeeping + error weights
                 ialth -= 1;
                 if (ialth == 0) {
                     // _order_step_control (ode.py:441-466)

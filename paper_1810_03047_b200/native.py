@@ -150,7 +150,7 @@ def fp64_peak_tflops(device: int = 0) -> float:
 
 
 PHASES = ("step-level", "predict", "gather", "spmv", "update", "reduction", "convergence",
-          "error-test/commit", "weights+order-control", "jump-test/jumps", "recording")
+          "error-test/commit", "order-control", "jump-test/jumps", "recording", "accept+weights")
 
 
 def phase_cycles():
