@@ -559,7 +559,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     CUDA_TRY(p->jump_t.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
     CUDA_TRY(p->jump_idx.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
     CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS + 1, s));
-    if (var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
+    if (var.reg_rows > 0 && var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
     CUDA_TRY(p->psum.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->psq.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));

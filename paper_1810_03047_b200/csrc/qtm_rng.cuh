@@ -71,7 +71,7 @@ struct Stream {
         }
     }
 
-    __device__ double next() {
+    __device__ __noinline__ double next() {
         const uint64_t i = n++;
         if (kind == kPhilox) {
             uint32_t c[4] = {(uint32_t)(i >> 2), (uint32_t)k, (uint32_t)(k >> 32), 0u};

@@ -28,6 +28,7 @@
 // powers from a Newton-refined root (the reference: glibc hypot/pow).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "qtm_rng.cuh"
 
@@ -133,13 +134,16 @@ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.
 // est ** (1/(q+1)) etc. in the step-size controller (ode.py:302, 445-453):
 // x > 0 and a small exponent, evaluated as exp2(y * log2(x)); within a few
 // ulp of the correctly rounded power, at a fraction of pow()'s latency.
-__device__ __forceinline__ double ctl_pow(double x, double y) {
+static __device__ __noinline__ double ctl_pow(double x, double y) {
     return x > 0.0 ? exp2(y * log2(x)) : (x == 0.0 ? 0.0 : pow(x, y));
 }
 
 // y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then
 // accumulated (reference _kernels.py:150-154, numba complex_mul).
-__device__ __forceinline__ double2 row_dot(const DevCsr& m, int i, const double2* __restrict__ x) {
+// not inlined: it serves the cold paths (recording of off-diagonal
+// observables, collapse channels, the non-staged fallback) and keeping a
+// single copy keeps the kernel's instruction footprint small
+static __device__ __noinline__ double2 row_dot(const DevCsr& m, int i, const double2* __restrict__ x) {
     double sr = 0.0, si = 0.0;
     const int b = __ldg(m.rp + i), en = __ldg(m.rp + i + 1);
     for (int j = b; j < en; ++j) {
@@ -249,6 +253,9 @@ struct Hist {
         __device__ __forceinline__ double2& at(int j, int e) const { return p[(j - RREG) * DP + e * (DP / E)]; }
     };
 
+    __device__ __forceinline__ static double2& at(Z& z, int j, int e) { return z[j][e]; }
+    __device__ __forceinline__ static const double2& at(const Z& z, int j, int e) { return z[j][e]; }
+
     // ---- order-specialised register paths (q + 1 <= RREG): straight-line
     // code, no per-row guards.  Dispatch by switch on the uniform order.
     template <int Q>
@@ -344,9 +351,6 @@ struct Hist {
 
     // inverse of predict (rejected attempt): passes r = q-1..0, j = r..q-1
     __device__ __forceinline__ static void undo(Z& z, const O& ovf, int q) {
-#define CALL_(Q) undo_q<Q>(z)
-        QTM_QSWITCH(CALL_)
-#undef CALL_
         for (int r = q - 1; r >= 0; --r) {
 #pragma unroll
             for (int j = 0; j < RREG - 1; ++j) {
@@ -370,9 +374,6 @@ struct Hist {
     // z[j] *= ratio^j, j = 1..q, ratio^j by repeated multiplication
     // (nordsieck_rescale, _kernels.py:107-114)
     __device__ __forceinline__ static void rescale(Z& z, const O& ovf, int q, double ratio) {
-#define CALL_(Q) rescale_q<Q>(z, ratio)
-        QTM_QSWITCH(CALL_)
-#undef CALL_
         double f = 1.0;
 #pragma unroll
         for (int j = 1; j < RREG; ++j) {
@@ -426,9 +427,6 @@ struct Hist {
 
     // psi(s) = Horner over rows q..0 (nordsieck_eval, _kernels.py:61-69)
     __device__ __forceinline__ static void horner(const Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
-#define CALL_(Q) horner_q<Q>(z, s, out)
-        QTM_QSWITCH(CALL_)
-#undef CALL_
 #pragma unroll
         for (int e = 0; e < E; ++e) out[e] = row(z, ovf, q, e);
         for (int j = q - 1; j >= RREG; --j) {
@@ -446,6 +444,71 @@ struct Hist {
 #undef QTM_QSWITCH
 };
 
+// ---------------------------------------- history in shared memory (RREG = 0)
+// Small-state variants keep all Nordsieck rows in shared memory: row j of
+// component e of thread t at p[j*DP + t + (DP/E)*e] (conflict-free, each
+// thread touches only its own column).  The operations become short runtime
+// loops, so the kernel's code stays small and its registers few -- this
+// regime (d <= ~100, one or a few warps per trajectory) is bound by
+// instruction fetch and latency, not by the row arithmetic.
+template <int E, int DP>
+struct HistS {
+    struct Z {
+        double2* p;
+    };
+    struct O {
+        double2* p;
+    };
+    __device__ __forceinline__ static double2& at(const Z& z, int j, int e) {
+        return z.p[j * DP + threadIdx.x + (DP / E) * e];
+    }
+    __device__ __forceinline__ static void predict(Z& z, const O&, int q) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            for (int r = 0; r < q; ++r) {
+                double2 carry = at(z, q, e);
+                for (int j = q - 1; j >= r; --j) {
+                    const double2 v = cadd(at(z, j, e), carry);
+                    at(z, j, e) = v;
+                    carry = v;
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ static void undo(Z& z, const O&, int q) {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            for (int r = q - 1; r >= 0; --r)
+                for (int j = r; j < q; ++j) at(z, j, e) = csub(at(z, j, e), at(z, j + 1, e));
+    }
+    __device__ __forceinline__ static void rescale(Z& z, const O&, int q, double ratio) {
+        double f = 1.0;
+        for (int j = 1; j <= q; ++j) {
+            f *= ratio;
+#pragma unroll
+            for (int e = 0; e < E; ++e) at(z, j, e) = cscale(f, at(z, j, e));
+        }
+    }
+    __device__ __forceinline__ static void commit(Z& z, const O&, int q, const double* l,
+                                                  const double2 (&ev)[E]) {
+        for (int j = 0; j <= q; ++j) {
+            const double lj = l[j];
+#pragma unroll
+            for (int e = 0; e < E; ++e) at(z, j, e) = cadd(at(z, j, e), cscale(lj, ev[e]));
+        }
+    }
+    __device__ __forceinline__ static double2 row(const Z& z, const O&, int j, int e) { return at(z, j, e); }
+    __device__ __forceinline__ static void set_row(Z& z, const O&, int j, int e, double2 v) { at(z, j, e) = v; }
+    __device__ __forceinline__ static void horner(const Z& z, const O&, int q, double s, double2 (&out)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double2 acc = at(z, q, e);
+            for (int j = q - 1; j >= 0; --j) acc = cadd(cscale(s, acc), at(z, j, e));
+            out[e] = acc;
+        }
+    }
+};
+
 // ------------------------------------------------------------- the kernel
 template <int NT, int E, int RREG>
 struct TrajKernel {
@@ -454,7 +517,8 @@ struct TrajKernel {
 
     // fixed part of the dynamic shared memory; the staged operator follows
     __host__ __device__ static constexpr size_t smem_bytes() {
-        return sizeof(double2) * (size_t)DP * 4 + sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1);
+        return sizeof(double2) * (size_t)DP * (RREG == 0 ? 4 + LROWS : 4) +
+               sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1);
     }
 };
 
@@ -481,7 +545,7 @@ template <int NT, int E, int RREG, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
 traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R) {
     constexpr int DP = NT * E;
-    using H = Hist<RREG, E, DP>;
+    using H = std::conditional_t<RREG == 0, HistS<E, DP>, Hist<(RREG > 0 ? RREG : 2), E, DP>>;
     extern __shared__ double2 smem[];
     // gath[2][DP]: double-buffered gather buffers; gath[gbuf] is the most
     //              recently published vector (the corrector iterate lives here)
@@ -490,6 +554,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     double2* const gath = smem;
     double2* const ebuf = smem + 2 * DP;
     double* const red = reinterpret_cast<double*>(smem + 4 * DP);
+    // RREG == 0: the Nordsieck rows follow the reduction scratch
+    double2* const zrows = reinterpret_cast<double2*>(
+        reinterpret_cast<char*>(smem) + sizeof(double2) * (size_t)DP * 4 + sizeof(double) * 2 * KRED * (NT / 32 > 1 ? NT / 32 : 1));
     __shared__ long long s_row;
     __shared__ long long s_stats[NSTATS];
     __shared__ Stream s_stream;
@@ -515,7 +582,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define ACT(e) (II(e) < d)
     // overflow column of this thread (rows >= RREG), rebuilt where used so it
     // holds no register across the hot loop
-#define OVF() (typename H::O{R.zovf + (size_t)blockIdx.x * (LROWS - RREG) * DP + tid})
+#define OVF() (typename H::O{R.zovf + (size_t)blockIdx.x * (RREG > 0 ? LROWS - RREG : 0) * DP + tid})
 
     // ---- stage G (sliced ELL + value dictionary) in shared memory once
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
@@ -566,7 +633,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         long long ph_last = clock64();
 #endif
 
-        double2 z[RREG][E];  // Nordsieck history rows 0..RREG-1 (registers)
+        typename H::Z z;  // Nordsieck history: registers (rows < RREG) or shared memory (RREG == 0)
+        if constexpr (RREG == 0) z.p = zrows;
         double w[E];         // error weights 1/(atol + rtol |z0_i|)
         double t, h, crate;
         int q, ialth;
@@ -669,9 +737,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         double2 f__[E];                                                      \
         GSPMV(xs__, f__);                                                    \
         _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
-            z[0][e] = (y0)[e];                                               \
-            z[1][e] = cscale(h, f__[e]);                                     \
-            _Pragma("unroll") for (int j = 2; j < RREG; ++j) z[j][e] = make_double2(0.0, 0.0); \
+            H::at(z, 0, e) = (y0)[e];                                        \
+            H::at(z, 1, e) = cscale(h, f__[e]);                              \
             w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
         }                                                                    \
         crate = 0.7; ialth = 2; has_eprev = false;                           \
@@ -713,7 +780,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     {
                         double2 y0p[E];
 #pragma unroll
-                        for (int e = 0; e < E; ++e) y0p[e] = z[0][e];
+                        for (int e = 0; e < E; ++e) y0p[e] = H::at(z, 0, e);
                         PH_MARK(1);  // [1] predict
                         GATHER(y0p, xs0);
                         PH_MARK(2);  // [2] gather z0 + barrier
@@ -731,7 +798,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         for (int e = 0; e < E; ++e) {
                             if (ACT(e)) {
                                 const double2 f = fg[e];
-                                const double2 z1 = z[1][e], z0 = z[0][e];
+                                const double2 z1 = H::at(z, 1, e), z0 = H::at(z, 0, e);
                                 const double2 ei = csub(cscale(h, f), z1);
                                 const double2 yn = cadd(z0, cscale(l0, ei));
                                 const double2 dd = csub(yn, cur[II(e)]);
@@ -788,13 +855,13 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         h *= 0.1;
                         double2 y0c[E];
 #pragma unroll
-                        for (int e = 0; e < E; ++e) y0c[e] = z[0][e];
+                        for (int e = 0; e < E; ++e) y0c[e] = H::at(z, 0, e);
                         GATHER(y0c, xs);
                         STAT(sNfe, 1);
                         double2 fr[E];
                         GSPMV(xs, fr);
 #pragma unroll
-                        for (int e = 0; e < E; ++e) z[1][e] = cscale(h, fr[e]);
+                        for (int e = 0; e < E; ++e) H::at(z, 1, e) = cscale(h, fr[e]);
                         has_eprev = false;
                         ialth = q + 1;
                     } else {
@@ -810,7 +877,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 ws.c_steps++;
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const double2 z0 = z[0][e];
+                    const double2 z0 = H::at(z, 0, e);
                     w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
                 }
                 PH_MARK(11);  // [11] accepted-step bookkeeping + error weights

@@ -242,3 +242,21 @@ def test_chunked_large_ensemble():
     np.testing.assert_array_equal(big.values[65_536:], tail.values)
     np.testing.assert_allclose(big.sum, big.values.sum(axis=0), rtol=1e-10, atol=1e-9)
     assert big.stats_total[0] == big.stats[:, 0].sum()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_shared_memory_history_variants_agree(name):
+    # variants keeping the Nordsieck rows in shared memory (reg_rows == 0)
+    # integrate the same trajectories as the register-resident ones
+    p = configs.build(name)
+    d = p.dim
+    vs = native.variants()
+    smem = [i for i, (t, e, r) in enumerate(vs) if r == 0 and t * e >= d]
+    regs = [i for i, (t, e, r) in enumerate(vs) if r > 0 and t * e >= d]
+    assert smem and regs
+    with DeviceProblem(p, variant=regs[0]) as ref, DeviceProblem(p, variant=smem[0]) as dp:
+        a = ref.run(7, 0, 64, max_jumps=MAXJ)
+        b = dp.run(7, 0, 64, max_jumps=MAXJ)
+    assert a.rc == 0 and b.rc == 0
+    np.testing.assert_array_equal(a.jump_count, b.jump_count)
+    np.testing.assert_allclose(a.values, b.values, rtol=0, atol=TOL)

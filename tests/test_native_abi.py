@@ -48,7 +48,7 @@ def test_host_queries_without_gpu():
     v = native.variants()
     assert len(v) >= 10
     for threads, comps, rows in v:
-        assert threads % 32 == 0 and comps >= 1 and 2 <= rows <= 13
+        assert threads % 32 == 0 and comps >= 1 and (rows == 0 or 2 <= rows <= 13)
     assert L.qtm_device_count() >= 0
 
 
