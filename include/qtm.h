@@ -149,6 +149,9 @@ typedef struct {
 int qtm_problem_create(const qtm_problem_desc* desc, qtm_problem** out);
 int qtm_run(qtm_problem* problem, const qtm_run_args* args, qtm_run_out* out);
 void qtm_problem_destroy(qtm_problem* problem);
+/* trajectories the problem's kernel variant keeps in flight on its device
+ * (SMs x resident CTAs per SM): the persistent grid of a large run */
+int qtm_max_resident(qtm_problem* problem, int32_t* ctas);
 
 /* Device-resident variant for benchmarking: results stay on the device;
  * only the per-point sums are copied out.  Same semantics as qtm_run. */

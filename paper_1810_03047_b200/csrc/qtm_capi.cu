@@ -506,6 +506,17 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
 
 void qtm_problem_destroy(qtm_problem* p) { free_problem(p); }
 
+int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
+    if (!p || !ctas) return set_error(QTM_ERR_ARGS, "null argument");
+    const Variant& var = variants()[p->variant];
+    int sms = 0, per_sm = 0;
+    CUDA_TRY(cudaSetDevice(p->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
+    *ctas = sms * per_sm;
+    return QTM_OK;
+}
+
 static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool copy_per_traj) {
     if (!p || !a || !o) return set_error(QTM_ERR_ARGS, "null argument");
     if (a->traj_end < a->traj_begin || a->traj_begin < 0) return set_error(QTM_ERR_ARGS, "bad trajectory range");

@@ -162,6 +162,13 @@ class DeviceProblem:
         self._handle = handle
         self._lock = threading.Lock()
 
+    def max_resident(self) -> int:
+        """Trajectories in flight at once (persistent grid size)."""
+        out = C.c_int32()
+        if native.lib().qtm_max_resident(self._handle, C.byref(out)) != 0:
+            raise RuntimeError(native.last_error())
+        return out.value
+
     def close(self):
         if getattr(self, "_handle", None):
             native.lib().qtm_problem_destroy(self._handle)
@@ -269,9 +276,13 @@ def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | No
     best, best_ms = -1, float("inf")
     for v in cands:
         with DeviceProblem(packed, device=device, variant=v) as dp:
-            out = dp.run(seed, 0, sample or 512, resident=True)
-        if out.kernel_ms < best_ms:
-            best, best_ms = v, out.kernel_ms
+            # enough trajectories for several waves of this variant's
+            # persistent grid, so the comparison is not decided by the tail
+            n = sample or min(max(6 * dp.max_resident(), 512), 8192)
+            out = dp.run(seed, 0, n, resident=True)
+        per_traj = out.kernel_ms / n
+        if per_traj < best_ms:
+            best, best_ms = v, per_traj
     _TUNED[key] = best
     return best
 
