@@ -344,6 +344,7 @@ def main(argv=None):
     peak = native.fp64_peak_tflops(local)
     achieved = flops / (k_ms * 1e-3) / 1e12
     hbm_equiv = bytes_model(st, packed) / (k_ms * 1e-3) / 1e9
+    layout = dp.layout()
     dp.close()
 
     # ---- end-to-end leg through the public API with host buffers ----------
@@ -392,7 +393,10 @@ def main(argv=None):
                        "failure_note": "reference-faithful OdeFailure(-5) step collapses, "
                                        "excluded from value and averages",
                        "kernel_variant": native.variants()[outs[-1].variant],
-                       "grid_ctas": outs[-1].grid},
+                       "grid_ctas": outs[-1].grid,
+                       "history_rows": {"registers": layout["reg_rows"],
+                                        "shared": layout["smem_rows"]},
+                       "smem_per_cta": layout["smem_bytes"]},
             "e2e": {"value": e2e_value, "unit": "trajectories/s",
                     "h2d_bytes_per_step": int(packed.nbytes()), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),

@@ -152,6 +152,11 @@ void qtm_problem_destroy(qtm_problem* problem);
 /* trajectories the problem's kernel variant keeps in flight on its device
  * (SMs x resident CTAs per SM): the persistent grid of a large run */
 int qtm_max_resident(qtm_problem* problem, int32_t* ctas);
+/* where the Nordsieck history lives for this problem's kernel variant: rows
+ * held in registers, rows in shared memory (the rest spill to global
+ * scratch), and the dynamic shared memory of one CTA */
+int qtm_problem_layout(qtm_problem* problem, int32_t* reg_rows, int32_t* smem_rows,
+                       int64_t* smem_bytes);
 
 /* Device-resident variant for benchmarking: results stay on the device;
  * only the per-point sums are copied out.  Same semantics as qtm_run. */

@@ -517,6 +517,15 @@ int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
     return QTM_OK;
 }
 
+int qtm_problem_layout(qtm_problem* p, int32_t* reg_rows, int32_t* smem_rows, int64_t* smem_bytes) {
+    if (!p || !reg_rows || !smem_rows || !smem_bytes) return set_error(QTM_ERR_ARGS, "null argument");
+    const Variant& var = variants()[p->variant];
+    *reg_rows = var.reg_rows > 0 ? std::min(var.reg_rows, LROWS) : 0;
+    *smem_rows = var.reg_rows > 0 ? 0 : LROWS;
+    *smem_bytes = (int64_t)p->smem;
+    return QTM_OK;
+}
+
 static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool copy_per_traj) {
     if (!p || !a || !o) return set_error(QTM_ERR_ARGS, "null argument");
     if (a->traj_end < a->traj_begin || a->traj_begin < 0) return set_error(QTM_ERR_ARGS, "bad trajectory range");

@@ -169,6 +169,14 @@ class DeviceProblem:
             raise RuntimeError(native.last_error())
         return out.value
 
+    def layout(self) -> dict:
+        """Nordsieck history placement: register rows, shared-memory rows
+        (the rest in global scratch) and dynamic shared memory per CTA."""
+        r, s, b = C.c_int32(), C.c_int32(), C.c_int64()
+        if native.lib().qtm_problem_layout(self._handle, C.byref(r), C.byref(s), C.byref(b)) != 0:
+            raise RuntimeError(native.last_error())
+        return {"reg_rows": r.value, "smem_rows": s.value, "smem_bytes": b.value}
+
     def close(self):
         if getattr(self, "_handle", None):
             native.lib().qtm_problem_destroy(self._handle)

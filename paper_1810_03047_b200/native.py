@@ -78,7 +78,7 @@ class QtmRunOut(C.Structure):
 
 
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",
-           "qtm_max_resident",
+           "qtm_max_resident", "qtm_problem_layout",
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
            "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles")
 
@@ -107,6 +107,8 @@ def lib():
     L.qtm_run_resident.restype = C.c_int
     L.qtm_max_resident.argtypes = [C.c_void_p, _I32P]
     L.qtm_max_resident.restype = C.c_int
+    L.qtm_problem_layout.argtypes = [C.c_void_p, _I32P, _I32P, C.POINTER(C.c_int64)]
+    L.qtm_problem_layout.restype = C.c_int
     L.qtm_problem_destroy.argtypes = [C.c_void_p]
     L.qtm_problem_destroy.restype = None
     L.qtm_last_error.argtypes = []
