@@ -329,6 +329,66 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
 
 // Dense copies of the observables that are diagonal (every stored entry on
 // the diagonal): the recording pass then reads one coalesced value per row.
+// Shared-memory copy of the real diagonal observables: per observable a byte
+// index per state component into a dictionary of its distinct values (a
+// number operator or sigma_z has a handful), so recording reads ~1 byte per
+// component from shared memory instead of 16 from L2.  Staged only when the
+// tables fit behind the operator without lowering the CTAs per SM.
+int stage_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp, const std::vector<double2>& dense) {
+    DevProblem& P = p->dp;
+    P.e_stage_mask = 0;
+    const int ne = d->n_expect;
+    if (!P.e_diag_mask || ne > MAXOPS) return QTM_OK;
+    std::vector<uint8_t> idx((size_t)ne * dp, 0);
+    std::vector<double> dict;
+    unsigned smask = 0;
+    for (int k = 0; k < ne; ++k) {
+        P.e_dict_off[k] = (int)dict.size();
+        if (!((P.e_diag_mask >> k) & 1u)) continue;
+        std::map<uint64_t, int> index;
+        std::vector<double> vals;
+        bool ok = true;
+        for (int i = 0; i < dp && ok; ++i) {
+            const double2 v = dense[(size_t)k * dp + i];
+            if (v.y != 0.0) { ok = false; break; }
+            uint64_t key;
+            memcpy(&key, &v.x, 8);
+            auto it = index.find(key);
+            if (it == index.end()) {
+                if (vals.size() >= 256) { ok = false; break; }
+                it = index.emplace(key, (int)vals.size()).first;
+                vals.push_back(v.x);
+            }
+            idx[(size_t)k * dp + i] = (uint8_t)it->second;
+        }
+        if (!ok) continue;
+        smask |= 1u << k;
+        dict.insert(dict.end(), vals.begin(), vals.end());
+    }
+    if (!smask) return QTM_OK;
+    const size_t off = (p->smem + 15) & ~(size_t)15;
+    const size_t idx_bytes = ((size_t)ne * dp + 15) & ~(size_t)15;
+    const size_t smem = off + idx_bytes + sizeof(double) * dict.size();
+    const Variant& var = variants()[p->variant];
+    int base = 0, occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&base, var.fn, var.threads, p->smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, var.threads, smem));
+    if (occ < 1 || occ < base) return QTM_OK;
+    idx.resize(idx_bytes, 0);
+    uint8_t* di = nullptr;
+    double* dd = nullptr;
+    CUDA_TRY(upload(p, &di, idx.data(), idx.size()));
+    CUDA_TRY(upload(p, &dd, dict.data(), dict.size()));
+    P.e_stage_mask = smask;
+    P.e_stage_off = (int)off;
+    P.e_stage_idx_bytes = (int)idx_bytes;
+    P.e_dict_n = (int)dict.size();
+    P.e_idx_g = di;
+    P.e_dict_g = dd;
+    p->smem = smem;
+    return QTM_OK;
+}
+
 int build_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp) {
     unsigned mask = 0;
     std::vector<double2> dense;
@@ -355,7 +415,7 @@ int build_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp) {
         CUDA_TRY(upload(p, &dd, dense.data(), dense.size()));
         p->dp.e_diag = dd;
     }
-    return QTM_OK;
+    return stage_expect_diag(p, d, dp, dense);
 }
 
 void free_problem(qtm_problem* p) {
@@ -485,14 +545,14 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     size_t static_smem = 4096;
     if (rc == QTM_OK && cudaFuncGetAttributes(&fattr, var.fn) == cudaSuccess) static_smem = fattr.sharedSizeBytes;
     const size_t dyn_cap = (size_t)smem_cap > static_smem ? (size_t)smem_cap - static_smem : 0;
+    if (rc == QTM_OK &&
+        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_cap) != cudaSuccess)
+        rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
     if (rc == QTM_OK) {
         bool staged = false;
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged);
     }
     if (rc == QTM_OK) rc = build_expect_diag(p, d, var.threads * var.comps);
-    if (rc == QTM_OK && p->smem > 48 * 1024 &&
-        cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_cap) != cudaSuccess)
-        rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
     if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
     if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "problem upload failed");

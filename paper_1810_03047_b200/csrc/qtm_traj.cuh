@@ -88,6 +88,16 @@ struct DevProblem {
     unsigned e_diag_mask;
     const double2* e_diag;
     int e_need_gather;      // some observable is not diagonal (needs all of psi)
+    // diagonal observables with real entries and <= 256 distinct values are
+    // staged in shared memory (bit k of e_stage_mask): a byte index per state
+    // component, idx[k * DP + i], into a per-observable value dictionary
+    // starting at entry e_dict_off[k]; the tables sit at byte offset
+    // e_stage_off of the dynamic shared memory (copied from e_idx_g/e_dict_g)
+    unsigned e_stage_mask;
+    int e_stage_off, e_stage_idx_bytes, e_dict_n;
+    int e_dict_off[MAXOPS];
+    const uint8_t* e_idx_g;
+    const double* e_dict_g;
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
     // per-order constants the reference evaluates inline, tabulated on the
@@ -588,6 +598,16 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
                                                        TrajKernel<NT, E, RREG>::smem_bytes());
     uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_dict + P.sell_dict_n);
+    // ---- stage the diagonal observables' index + dictionary tables
+    const uint8_t* const s_eidx = reinterpret_cast<const uint8_t*>(smem) + P.e_stage_off;
+    const double* const s_edict = reinterpret_cast<const double*>(s_eidx + P.e_stage_idx_bytes);
+    if (P.e_stage_mask) {
+        uint8_t* const di = reinterpret_cast<uint8_t*>(smem) + P.e_stage_off;
+        double* const dd = reinterpret_cast<double*>(di + P.e_stage_idx_bytes);
+        const uint32_t* const si = reinterpret_cast<const uint32_t*>(P.e_idx_g);
+        for (int i = tid; i < P.e_stage_idx_bytes / 4; i += NT) reinterpret_cast<uint32_t*>(di)[i] = si[i];
+        for (int i = tid; i < P.e_dict_n; i += NT) dd[i] = P.e_dict_g[i];
+    }
     int goff[E], gwidth = 0;
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
@@ -702,7 +722,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             _Pragma("unroll") for (int kk = 0; kk < KRED; ++kk) {            \
                 const int k = k0 + kk;                                       \
                 double acc__ = 0.0;                                          \
-                if (k < P.ne) {                                              \
+                if (k < P.ne && ((P.e_stage_mask >> k) & 1u)) {             \
+                    /* staged real diagonal: sum_i E_ii |psi_i|^2 */         \
+                    const double* const dk__ = s_edict + P.e_dict_off[k];    \
+                    _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) \
+                        acc__ += dk__[s_eidx[k * DP + II(e)]] * cabs2(psi[e]); \
+                } else if (k < P.ne) {                                       \
                     const bool dg__ = (P.e_diag_mask >> k) & 1u;             \
                     _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) { \
                         double2 s;                                           \
