@@ -170,7 +170,16 @@ static __device__ __noinline__ double2 row_dot(const DevCsr& m, int i, const dou
 // order (entries k ascending), so the rounding matches row_dot exactly.
 // Entry = x byte offset (col*16, low half) | dictionary byte offset (high
 // half), so each entry costs two 16-byte shared loads and no index math.
-template <int NT, int E>
+// Software-pipelined: the entries of column k+1 (PF >= 1) and the operands of
+// column k+1 (PF >= 2) are loaded while column k is multiplied, so one
+// shared-memory round trip per column overlaps the arithmetic.
+// PF = 2 costs 4E registers more than PF = 1 and loses to it wherever
+// registers are tight; the compact shared-history variants (RREG = 0) keep
+// the plain loop (their code size matters more than the load latency).
+#ifndef QTM_SPMV_PF
+#define QTM_SPMV_PF(RREG) ((RREG) == 0 ? 0 : 1)
+#endif
+template <int NT, int E, int PF>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
                                           const double2* __restrict__ dict, const int (&off)[E],
                                           int width, const double2* __restrict__ x,
@@ -181,15 +190,65 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
     double sr[E], si[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
+    if constexpr (PF == 0) {
 #pragma unroll (E >= 4 ? 1 : 2)
-    for (int k = 0; k < width; ++k) {
+        for (int k = 0; k < width; ++k) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const uint32_t u = ent[off[e] + k * 32 + lane];
+                const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
+                const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
+                sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
+                si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
+            }
+        }
+    } else if constexpr (PF == 1) {
+        uint32_t u[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) u[e] = ent[off[e] + lane];
+        for (int k = 0; k < width; ++k) {
+            const int kn = k + 1 < width ? k + 1 : k;
+            double2 v[E], xv[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                v[e] = *reinterpret_cast<const double2*>(db + (u[e] >> 16));
+                xv[e] = *reinterpret_cast<const double2*>(xb + (u[e] & 0xFFFFu));
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) u[e] = ent[off[e] + kn * 32 + lane];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                sr[e] = sr[e] + (v[e].x * xv[e].x - v[e].y * xv[e].y);
+                si[e] = si[e] + (v[e].x * xv[e].y + v[e].y * xv[e].x);
+            }
+        }
+    } else {
+        uint32_t u[E];
+        double2 v[E], xv[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const uint32_t u = ent[off[e] + k * 32 + lane];
-            const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
-            const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
-            sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
-            si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
+            const uint32_t u0 = ent[off[e] + lane];
+            v[e] = *reinterpret_cast<const double2*>(db + (u0 >> 16));
+            xv[e] = *reinterpret_cast<const double2*>(xb + (u0 & 0xFFFFu));
+            u[e] = ent[off[e] + (width > 1 ? 32 : 0) + lane];
+        }
+        for (int k = 0; k < width; ++k) {
+            const int k2 = k + 2 < width ? k + 2 : width - 1;
+            double2 vn[E], xn[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                vn[e] = *reinterpret_cast<const double2*>(db + (u[e] >> 16));
+                xn[e] = *reinterpret_cast<const double2*>(xb + (u[e] & 0xFFFFu));
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) u[e] = ent[off[e] + k2 * 32 + lane];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                sr[e] = sr[e] + (v[e].x * xv[e].x - v[e].y * xv[e].y);
+                si[e] = si[e] + (v[e].x * xv[e].y + v[e].y * xv[e].x);
+                v[e] = vn[e];
+                xv[e] = xn[e];
+            }
         }
     }
 #pragma unroll
@@ -622,7 +681,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV(xs, f)                                                         \
     do {                                                                     \
         if (P.sell_mode) {                                                   \
-            sell_spmv<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f);          \
+            sell_spmv<NT, E, QTM_SPMV_PF(RREG)>(s_ent, s_dict, goff, gwidth, (xs), f); \
         } else {                                                             \
             _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
                 f[e] = ACT(e) ? row_dot(P.g, II(e), (xs)) : make_double2(0.0, 0.0); \
