@@ -25,7 +25,7 @@
 // WRMS norms multiply by host-computed reciprocals of d and tau instead of
 // dividing (FP64 division sits on the per-attempt critical path),
 // hypot comes from CUDA's libdevice and the controller's fractional
-// powers from a Newton-refined root (the reference: glibc hypot/pow).
+// powers are exp2(y log2 x) (the reference: glibc hypot/pow).
 #pragma once
 #include <cstdint>
 #include <type_traits>
