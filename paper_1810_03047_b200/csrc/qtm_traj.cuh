@@ -587,7 +587,7 @@ struct TrajKernel {
     // fixed part of the dynamic shared memory; the staged operator follows
     __host__ __device__ static constexpr size_t smem_bytes() {
         return sizeof(double2) * (size_t)DP * (RREG == 0 ? 4 + LROWS : 4) +
-               sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1);
+               sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1) + sizeof(double) * (size_t)DP;
     }
 };
 
@@ -623,9 +623,11 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     double2* const gath = smem;
     double2* const ebuf = smem + 2 * DP;
     double* const red = reinterpret_cast<double*>(smem + 4 * DP);
-    // RREG == 0: the Nordsieck rows follow the reduction scratch
-    double2* const zrows = reinterpret_cast<double2*>(
-        reinterpret_cast<char*>(smem) + sizeof(double2) * (size_t)DP * 4 + sizeof(double) * 2 * KRED * (NT / 32 > 1 ? NT / 32 : 1));
+    // wsm[DP]: error weights 1/(atol + rtol |z0_i|), thread-private slots
+    // (read once per corrector iteration; kept out of the register file)
+    double* const wsm = red + 2 * KRED * (NT / 32 > 1 ? NT / 32 : 1);
+    // RREG == 0: the Nordsieck rows follow the weights
+    double2* const zrows = reinterpret_cast<double2*>(wsm + DP);
     __shared__ long long s_row;
     __shared__ long long s_stats[NSTATS];
     __shared__ Stream s_stream;
@@ -635,7 +637,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     // touches its own copy, so no barrier is involved).  Keeping them out of
     // the register file leaves the registers to the Nordsieck history.
     struct WarpCold {
-        double t_lo, r_thr;
+        double t_lo, r_thr, crate;
         long long row, steps_in_segment, njumps;
         int gi, nef, ncf;
         unsigned c_att, c_q, c_qq, c_it, c_steps;
@@ -714,8 +716,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 
         typename H::Z z;  // Nordsieck history: registers (rows < RREG) or shared memory (RREG == 0)
         if constexpr (RREG == 0) z.p = zrows;
-        double w[E];         // error weights 1/(atol + rtol |z0_i|)
-        double t, h, crate;
+#define W(e) wsm[II(e)]
+        double t, h;
         int q, ialth;
         bool has_eprev;
 
@@ -823,9 +825,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
             H::at(z, 0, e) = (y0)[e];                                        \
             H::at(z, 1, e) = cscale(h, f__[e]);                              \
-            w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
+            W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
         }                                                                    \
-        crate = 0.7; ialth = 2; has_eprev = false;                           \
+        ws.crate = 0.7; ialth = 2; has_eprev = false;                        \
     } while (0)
 
         t = P.t_from;
@@ -886,8 +888,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 const double2 ei = csub(cscale(h, f), z1);
                                 const double2 yn = cadd(z0, cscale(l0, ei));
                                 const double2 dd = csub(yn, cur[II(e)]);
-                                v[0] += cabs2(dd) * w[e] * w[e];
-                                v[1] += cabs2(ei) * w[e] * w[e];
+                                const double we = W(e);
+                                v[0] += cabs2(dd) * we * we;
+                                v[1] += cabs2(ei) * we * we;
                                 v[2] += cabs2(yn);
                                 nxt[II(e)] = yn;
                                 ecurp[II(e)] = ei;
@@ -902,10 +905,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         acc_e = v[1];
                         nrm2 = v[2];
                         if (m > 0) {
-                            const double a = 0.2 * crate, b = del / delp;
-                            crate = b > a ? b : a;
+                            const double a = 0.2 * ws.crate, b = del / delp;
+                            ws.crate = b > a ? b : a;
                         }
-                        const double c15 = 1.5 * crate;
+                        const double c15 = 1.5 * ws.crate;
                         if (del * (c15 < 1.0 ? c15 : 1.0) <= conit) { converged = true; break; }
                         if (m > 0 && del > 2.0 * delp) break;
                         delp = del;
@@ -962,7 +965,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = H::at(z, 0, e);
-                    w[e] = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
+                    W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
                 }
                 PH_MARK(11);  // [11] accepted-step bookkeeping + error weights
                 ialth -= 1;
@@ -979,8 +982,9 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                             if (ACT(e)) {
                                 const double2 zq = H::row(z, OVF(), q, e);
                                 const double2 de = csub(ecp[II(e)], epp[II(e)]);
-                                v[0] += cabs2(zq) * w[e] * w[e];
-                                v[1] += cabs2(de) * w[e] * w[e];
+                                const double we = W(e);
+                                v[0] += cabs2(zq) * we * we;
+                                v[1] += cabs2(de) * we * we;
                             }
                         }
                     }
@@ -1150,6 +1154,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         __syncthreads();
     }
 #undef OVF
+#undef W
 #undef II
 #undef ACT
 #undef GATHER
