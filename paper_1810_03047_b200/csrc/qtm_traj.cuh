@@ -98,6 +98,11 @@ struct DevProblem {
     int e_dict_off[MAXOPS];
     const uint8_t* e_idx_g;
     const double* e_dict_g;
+    // e_fast: every observable is staged (recording takes the transposed
+    // warp reduction); e_stage_dense: the staged table is the dense real
+    // diagonal [ne][DP] (doubles, copied from e_dense_g) instead of bytes
+    int e_fast, e_stage_dense;
+    const double* e_dense_g;
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
     // per-order constants the reference evaluates inline, tabulated on the
@@ -305,6 +310,66 @@ __device__ __forceinline__ void warp_sum_lane0(double (&v)[K]) {
     for (int m = 16; m >= 1; m >>= 1) {
 #pragma unroll
         for (int k = 0; k < K; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], m);
+    }
+}
+
+// One lane-halving level of a multi-value warp reduction: lanes with bit m
+// clear keep the first half of a[0..N), the others the second half, and
+// each adds its partner's copy of the half it keeps (a fixed order, so the
+// result is deterministic).  After log2(N) levels lane l holds value slot
+// (bits of l selected by the masks) summed over the lanes that agree with
+// it in those bits.
+template <int N>
+__device__ __forceinline__ void warp_halve(double (&a)[8], int m) {
+    const bool upper = (threadIdx.x & m) != 0;
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+        const double send = upper ? a[j] : a[j + N / 2];
+        const double keep = upper ? a[j + N / 2] : a[j];
+        a[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+}
+
+// Recording when every observable is a staged real diagonal: per warp the
+// partial <psi|E_k|psi> = sum_i E_k(i) |psi_i|^2 for k < ne and <psi|psi>
+// (slot ne), in groups of 8 slots.  The 8 per-lane values of a group are
+// reduced by three halving levels (16, 8, 4) and two butterflies (2, 1):
+// 18 shuffles for 8 values instead of 80; lanes 4j' store the slots.
+template <int NT, int E, bool DENSE>
+__device__ __forceinline__ void record_staged(const DevProblem& P, const double2* smem,
+                                              const double (&pw)[E], double* rp) {
+    constexpr int DP = NT * E;
+    const int lane = threadIdx.x & 31;
+    const char* const base = reinterpret_cast<const char*>(smem) + P.e_stage_off;
+    const double* const dense = reinterpret_cast<const double*>(base) + threadIdx.x;
+    const uint8_t* const idx = reinterpret_cast<const uint8_t*>(base) + threadIdx.x;
+    const double* const dict = reinterpret_cast<const double*>(base + P.e_stage_idx_bytes);
+    for (int g = 0; g <= P.ne; g += 8) {
+        double a[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = g + j;
+            double acc = 0.0;
+            if (k < P.ne) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const double v = DENSE ? dense[k * DP + NT * e]
+                                           : dict[P.e_dict_off[k] + idx[k * DP + NT * e]];
+                    acc += v * pw[e];
+                }
+            } else if (k == P.ne) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc += pw[e];
+            }
+            a[j] = acc;
+        }
+        warp_halve<8>(a, 16);
+        warp_halve<4>(a, 8);
+        warp_halve<2>(a, 4);
+        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+        const int slot = g + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        if ((lane & 3) == 0 && slot <= P.ne) rp[(size_t)slot * (NT / 32)] = a[0];
     }
 }
 
@@ -662,7 +727,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     // ---- stage the diagonal observables' index + dictionary tables
     const uint8_t* const s_eidx = reinterpret_cast<const uint8_t*>(smem) + P.e_stage_off;
     const double* const s_edict = reinterpret_cast<const double*>(s_eidx + P.e_stage_idx_bytes);
-    if (P.e_stage_mask) {
+    if (P.e_stage_dense) {
+        double* const dd = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + P.e_stage_off);
+        for (int i = tid; i < P.ne * DP; i += NT) dd[i] = P.e_dense_g[i];
+    } else if (P.e_stage_mask) {
         uint8_t* const di = reinterpret_cast<uint8_t*>(smem) + P.e_stage_off;
         double* const dd = reinterpret_cast<double*>(di + P.e_stage_idx_bytes);
         const uint32_t* const si = reinterpret_cast<const uint32_t*>(P.e_idx_g);
@@ -776,6 +844,15 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         }                                                                    \
         double* const rp__ = R.rec_partial +                                 \
             ((size_t)ws.row * npts + (gi_)) * (size_t)(P.ne + 1) * (NT / 32) + (tid >> 5); \
+        if (RREG > 0 && P.e_fast) { /* (RREG = 0: compact code wins) */     \
+            double pw__[E];                                                  \
+            _Pragma("unroll") for (int e = 0; e < E; ++e) pw__[e] = ACT(e) ? cabs2(psi[e]) : 0.0; \
+            if (P.e_stage_dense)                                             \
+                record_staged<NT, E, true>(P, smem, pw__, rp__);             \
+            else                                                             \
+                record_staged<NT, E, false>(P, smem, pw__, rp__);            \
+            break;                                                           \
+        }                                                                    \
         double nrm__ = 0.0;                                                  \
         _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) nrm__ += cabs2(psi[e]); \
         for (int k0 = 0; k0 <= P.ne; k0 += KRED) {                           \
