@@ -543,6 +543,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         P.inv_tau1[q] = P.tau1[q] != 0.0 ? 1.0 / P.tau1[q] : 0.0;
         P.inv_tau2[q] = P.tau2[q] != 0.0 ? 1.0 / P.tau2[q] : 0.0;
         P.inv_tau3[q] = P.tau3[q] != 0.0 ? 1.0 / P.tau3[q] : 0.0;
+        const double lim = 1.0 / 1.1 - 1e-6;  // r < 1.1  <=>  bias * est^(1/k) > lim
+        P.keep_same[q] = std::pow(lim / 1.2, q + 1);
+        P.keep_down[q] = std::pow(lim / 1.3, q);
+        P.keep_up[q] = std::pow(lim / 1.4, q + 2);
     }
     P.inv_d = 1.0 / (double)d->dim;
     rc = upload_csr(p, d->generator, d->dim, &P.g, "generator");

@@ -112,6 +112,10 @@ struct DevProblem {
     // sqrt(acc * inv_d) * inv_tau (last-bit differences only)
     double inv_d;
     double inv_tau1[LROWS], inv_tau2[LROWS], inv_tau3[LROWS];
+    // order control keeps q and h (every ratio < 1.1) iff est > keep_same[q],
+    // est_down > keep_down[q] (when q > 1) and est_up > keep_up[q] (when
+    // raising is possible): ((1/1.1 - 1e-6) / bias)^k, k = q+1, q, q+2
+    double keep_same[LROWS], keep_down[LROWS], keep_up[LROWS];
 };
 
 struct RunParams {
@@ -863,8 +867,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 if (k < P.ne && ((P.e_stage_mask >> k) & 1u)) {             \
                     /* staged real diagonal: sum_i E_ii |psi_i|^2 */         \
                     const double* const dk__ = s_edict + P.e_dict_off[k];    \
+                    const double* const dd__ = reinterpret_cast<const double*>(s_eidx); \
                     _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) \
-                        acc__ += dk__[s_eidx[k * DP + II(e)]] * cabs2(psi[e]); \
+                        acc__ += (P.e_stage_dense ? dd__[k * DP + II(e)]        \
+                                                  : dk__[s_eidx[k * DP + II(e)]]) * cabs2(psi[e]); \
                 } else if (k < P.ne) {                                       \
                     const bool dg__ = (P.e_diag_mask >> k) & 1u;             \
                     _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) { \
@@ -1066,10 +1072,20 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         }
                     }
                     block_sum<NT, 2>(v, red, rphase);
-                    // the three candidate ratios are independent: straight-line
-                    // code so their powers overlap (unused ones are discarded)
                     const double est_d = sqrt(v[0] * P.inv_d) * P.inv_tau1[q];
                     const double est_u = sqrt(v[1] * P.inv_d) * P.inv_tau3[q];
+                    // every candidate ratio below 1.1 <=> every estimate above
+                    // its host-tabulated threshold (r = 1/(c est^(1/k) + 1e-6)
+                    // is decreasing in est): keep order and step without
+                    // evaluating the three powers -- the common outcome
+                    if (est > P.keep_same[q] && (!need_d || est_d > P.keep_down[q]) &&
+                        (!need_u || est_u > P.keep_up[q])) {
+                        ialth = 3;
+                        ecur ^= 1;  // e_prev = e
+                        has_eprev = true;
+                        goto order_done;
+                    }
+                    {
                     const double r_same = __drcp_rn(1.2 * ctl_pow(est, P.rq1[q]) + 1e-6);
                     const double pd = __drcp_rn(1.3 * ctl_pow(est_d, P.rq0[q]) + 1e-6);
                     const double pu = __drcp_rn(1.4 * ctl_pow(est_u, P.rq2[q]) + 1e-6);
@@ -1098,6 +1114,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         const double m1 = 10.0 < best ? 10.0 : best;
                         RESCALE(m1 > 0.1 ? m1 : 0.1);
                     }
+                    }
+                order_done:;
                 } else {
                     ecur ^= 1;  // e_prev = e
                     has_eprev = true;

@@ -193,6 +193,34 @@ def test_no_support_raises_value_error():
         run_gpu(p, 2, 3)
 
 
+def _observable_mix(kind):
+    """c1's dynamics with observables that exercise each recording path."""
+    from paper_1810_03047_b200.qops import sigma_x
+    sm = sigma_minus()
+    obs = {"real_diag": (sigma_z(), sm.conj().T @ sm),              # staged (dense/bytes)
+           "off_diag": (sigma_z(), sigma_x()),                      # gather + CSR row dot
+           "complex_diag": (sigma_z(), np.diag([1.0 + 2.0j, -0.5j]))}[kind]  # global dense
+    ops = OperatorSet(0.5 * sigma_x(), (np.sqrt(0.1) * sm,), obs)
+    return QuantumProblem.from_operators(ops, fock(2, 0), 0.0, 20.0, 200,
+                                         OdeConfig(rtol=1e-8, atol=1e-10))
+
+
+@pytest.mark.parametrize("kind", ["real_diag", "off_diag", "complex_diag"])
+@pytest.mark.parametrize("variant", [0, 17])  # register history / shared-memory history
+def test_recording_paths_match_oracle(kind, variant, oracle_lib):
+    pk = pack_problem(_observable_mix(kind))
+    with DeviceProblem(pk, variant=variant) as dp:
+        out = dp.run(goldens.SEED, 0, 64, max_jumps=MAXJ)
+    ref = oracle_lib.run(pk, goldens.SEED, 0, 64, max_jumps=MAXJ)
+    assert out.rc == 0 and ref["rc"] == 0
+    np.testing.assert_array_equal(out.jump_count, ref["jump_count"])
+    # the dynamics agree to rounding-level drift (c1 sits at ~1e-7, see the
+    # identical-stream test); the recording paths themselves are exact
+    np.testing.assert_allclose(out.values, ref["values"], rtol=0, atol=TOL)
+    np.testing.assert_allclose(out.sum / 64, ref["values"].mean(axis=0), rtol=0, atol=TOL)
+    np.testing.assert_array_equal(out.values[:, :, 0], ref["values"][:, :, 0])  # from psi0
+
+
 @pytest.mark.parametrize("variant", range(len(native.variants())))
 def test_large_variants_agree(variant):
     # every d=1024-capable kernel variant (register row budgets 4..10, with
