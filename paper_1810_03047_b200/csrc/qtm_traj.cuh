@@ -264,41 +264,71 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
     for (int e = 0; e < E; ++e) out[e] = make_double2(sr[e], si[e]);
 }
 
-// Bitwise-identical sums on every thread of the CTA: xor-butterfly inside
-// each warp (a+b == b+a at every level, so all lanes agree), lane 0 of every
-// warp publishes its partial, then every warp loads the NW partials one per
-// lane and runs the same butterfly -- identical data and order in every warp.
-// Double-buffered scratch => one barrier per reduction.
+// One lane-halving level of a multi-value warp reduction: lanes with bit m
+// clear keep the first half of a[0..N), the others the second half, and
+// each adds its partner's copy of the half it keeps (a fixed order, so the
+// result is deterministic).  After log2(N) levels lane l holds value slot
+// (bits of l selected by the masks) summed over the lanes that agree with
+// it in those bits.
+template <int N, int S>
+__device__ __forceinline__ void warp_halve(double (&a)[S], int m) {
+    const bool upper = (threadIdx.x & m) != 0;
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+        const double send = upper ? a[j] : a[j + N / 2];
+        const double keep = upper ? a[j + N / 2] : a[j];
+        a[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+}
+
+// Bitwise-identical sums on every thread of the CTA.  Inside each warp the K
+// values are reduced by halving levels (each lane keeps half of the slots it
+// still holds) and then butterflies, so K = 3 costs 12 shuffles instead of
+// 30; the lanes holding a finished slot publish it; after ONE barrier every
+// thread adds the NW warp partials of each slot in warp order -- the same
+// data in the same order everywhere.  Double-buffered scratch => one
+// barrier per reduction.  (One warp: plain xor-butterfly, all lanes agree.)
 template <int NT, int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& phase) {
+    static_assert(K >= 1 && K <= KRED, "block_sum carries at most KRED values");
+    if constexpr (NT == 32) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < K; ++k) {
 #pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], m);
-    }
-    if constexpr (NT > 32) {
+            for (int m = 16; m >= 1; m >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], m);
+        }
+    } else {
         constexpr int NW = NT / 32;
         double* buf = red + phase * (KRED * NW);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (lane == 0) {
+        if constexpr (K == 1) {
+            double s = v[0];
 #pragma unroll
-            for (int k = 0; k < K; ++k) buf[k * NW + warp] = v[k];
+            for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+            if (lane == 0) buf[warp] = s;
+        } else if constexpr (K == 2) {
+            double a[2] = {v[0], v[1]};
+            warp_halve<2>(a, 16);
+#pragma unroll
+            for (int m = 8; m >= 1; m >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], m);
+            if ((lane & 15) == 0) buf[(lane >> 4) * NW + warp] = a[0];
+        } else {
+            double a[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) a[k] = k < K ? v[k] : 0.0;
+            warp_halve<4>(a, 16);
+            warp_halve<2>(a, 8);
+#pragma unroll
+            for (int m = 4; m >= 1; m >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], m);
+            const int slot = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+            if ((lane & 7) == 0 && slot < K) buf[slot * NW + warp] = a[0];
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            double s;
-            if constexpr ((NW & (NW - 1)) == 0) {
-                // power-of-two warp count: every lane loads partial lane % NW,
-                // log2(NW) butterfly levels leave the total in all lanes
-                s = buf[k * NW + (lane & (NW - 1))];
+            double s = buf[k * NW];
 #pragma unroll
-                for (int m = NW / 2; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-            } else {
-                s = lane < NW ? buf[k * NW + lane] : 0.0;
-#pragma unroll
-                for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-            }
+            for (int w = 1; w < NW; ++w) s += buf[k * NW + w];
             v[k] = s;
         }
         phase ^= 1;
@@ -314,23 +344,6 @@ __device__ __forceinline__ void warp_sum_lane0(double (&v)[K]) {
     for (int m = 16; m >= 1; m >>= 1) {
 #pragma unroll
         for (int k = 0; k < K; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], m);
-    }
-}
-
-// One lane-halving level of a multi-value warp reduction: lanes with bit m
-// clear keep the first half of a[0..N), the others the second half, and
-// each adds its partner's copy of the half it keeps (a fixed order, so the
-// result is deterministic).  After log2(N) levels lane l holds value slot
-// (bits of l selected by the masks) summed over the lanes that agree with
-// it in those bits.
-template <int N>
-__device__ __forceinline__ void warp_halve(double (&a)[8], int m) {
-    const bool upper = (threadIdx.x & m) != 0;
-#pragma unroll
-    for (int j = 0; j < N / 2; ++j) {
-        const double send = upper ? a[j] : a[j + N / 2];
-        const double keep = upper ? a[j + N / 2] : a[j];
-        a[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
 }
 

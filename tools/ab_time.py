@@ -12,6 +12,7 @@ for spec in sys.argv[1:]:
     pk = pack_problem(configs.build(name))
     with DeviceProblem(pk, variant=int(v)) as dp:
         dp.run(1, 0, min(int(n), 256), resident=True)
-        ts = [dp.run(987654321, 0, int(n), resident=True).kernel_ms for _ in range(2)]
+        outs = [dp.run(987654321, 0, int(n), resident=True) for _ in range(2)]
+    ts = [o.kernel_ms for o in outs]
     print(f"{lib:18s} {name} n={n} v={native.variants()[int(v)] if int(v) >= 0 else 'auto'} "
-          f"kernel_ms {min(ts):9.2f}", flush=True)
+          f"kernel_ms {min(ts):9.2f} attempts {int(outs[0].stats_total[0])}", flush=True)
