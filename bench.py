@@ -178,12 +178,15 @@ CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1}
 
 
 def profiled_traffic(config: str):
-    """DRAM bytes per launch of the trajectory kernel from the committed ncu
-    --set full capture of this config (profiles/r01_<config>_traj_kernel_raw_selected.csv),
-    or None when there is none."""
-    path = os.path.join(REPO, "profiles", f"r01_{config}_traj_kernel_raw_selected.csv")
-    if not os.path.exists(path):
+    """DRAM bytes per launch of the trajectory kernel from the newest committed
+    ncu --set full capture of this config
+    (profiles/r<NN>_<config>_traj_kernel_raw_selected.csv), or None."""
+    import glob
+    found = sorted(glob.glob(os.path.join(REPO, "profiles",
+                                          f"r[0-9][0-9]_{config}_traj_kernel_raw_selected.csv")))
+    if not found:
         return None
+    path = found[-1]
     vals = {}
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     with open(path) as f:
