@@ -21,6 +21,20 @@
  *   - apply_collapse ................................... trajectory.py:133-154
  *   - record / record_expectation ...................... trajectory.py:122-130, 206-214
  *   - run_single_trajectory ............................ trajectory.py:190-250
+ *   BDF (method = MO_METHOD_BDF, the general engine with a CSR generator):
+ *   - _attempt_general (save, predict, Newton, error test,
+ *     commit / restore) ................................. ode.py:334-356
+ *   - _newton_correct (modified Newton, <= 3 iterations,
+ *     one retry with a fresh iteration matrix) ......... ode.py:379-407
+ *   - _ensure_iteration_matrix (refactor when |h l0 / h l0_fact - 1| > 0.3,
+ *     stale, or no LU; M = I - h l0 J, J = G) ........... ode.py:409-423
+ *   - scipy lu_factor / lu_solve = LAPACK zgetrf / zgetrs, restated as the
+ *     unblocked right-looking LU with partial pivoting (pivot = first row of
+ *     maximal |re| + |im|, izamax), row swaps, reciprocal scaling of the
+ *     sub-column and the rank-1 update; then the row interchanges and the
+ *     unit-lower / upper triangular solves (column-oriented, ztrsm order).
+ *     OpenBLAS blocks the trailing update differently, so agreement with
+ *     the reference is at the rounding level here, not bitwise.
  * with the same summation orders (rows left to right, components in index
  * order) and no FMA contraction (build with -ffp-contract=off, as numba's
  * default non-fastmath LLVM lowering).  Two places use numpy/BLAS in the
@@ -60,6 +74,23 @@ static inline cplx csub(cplx a, cplx b) { cplx r = {a.re - b.re, a.im - b.im}; r
 static inline cplx cscale(double s, cplx a) { cplx r = {s * a.re, s * a.im}; return r; }
 static inline double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
 static inline double cabs_(cplx a) { return hypot(a.re, a.im); }
+static inline double cabs1(cplx a) { return fabs(a.re) + fabs(a.im); }
+/* a / b in numpy's order (Smith's algorithm, npymath complex divide) */
+static inline cplx cdiv(cplx a, cplx b) {
+    double abr = fabs(b.re), abi = fabs(b.im);
+    cplx r;
+    if (abr >= abi) {
+        if (abr == 0.0 && abi == 0.0) { r.re = a.re / abr; r.im = a.im / abr; return r; }
+        double rat = b.im / b.re, scl = 1.0 / (b.re + b.im * rat);
+        r.re = (a.re + a.im * rat) * scl;
+        r.im = (a.im - a.re * rat) * scl;
+    } else {
+        double rat = b.re / b.im, scl = 1.0 / (b.im + b.re * rat);
+        r.re = (a.re * rat + a.im) * scl;
+        r.im = (a.im * rat - a.re) * scl;
+    }
+    return r;
+}
 
 /* ---------------------------------------------------------------- streams */
 #define M32 0xFFFFFFFFu
@@ -248,6 +279,13 @@ typedef struct {
     int ialth;
     int has_eprev;
     cplx *z, *zp, *e, *eprev, *ycur, *f, *psi, *work;
+    /* BDF: saved history rows, predicted y and z1, Newton step, iteration
+     * matrix LU (column-major n x n) with its pivots, squared weights */
+    cplx *save, *ypred, *z1pred, *dy, *lu;
+    int64_t* ipiv;
+    double* w2;
+    int has_lu, jac_stale;
+    double hl0_fact;
     /* stats */
     int64_t* st;
 } solver_t;
@@ -321,6 +359,165 @@ static double step_kernel(solver_t* S, int* status) {
     return est;
 }
 
+/* ------------------------------------------------------------ BDF engine */
+/* M = I - hl0 G built from the CSR generator (ode.py:418-420: -hl0 * jac,
+ * then += 1 on the diagonal), factored in place: column-major LU with
+ * partial pivoting (zgetf2 order). */
+static void bdf_factor(solver_t* S, double hl0) {
+    const mo_problem* P = S->P;
+    int64_t n = S->n;
+    cplx* a = S->lu;
+    const cplx* gv = (const cplx*)P->g.values;
+    memset(a, 0, sizeof(cplx) * n * n);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = P->g.row_ptr[i]; j < P->g.row_ptr[i + 1]; ++j)
+            a[P->g.col_ind[j] * n + i] = cscale(-hl0, gv[j]);
+    for (int64_t i = 0; i < n; ++i) a[i * n + i].re += 1.0;
+    for (int64_t k = 0; k < n; ++k) {
+        cplx* ck = a + k * n;
+        int64_t p = k;
+        double best = cabs1(ck[k]);
+        for (int64_t i = k + 1; i < n; ++i) {
+            double v = cabs1(ck[i]);
+            if (v > best) { best = v; p = i; }
+        }
+        S->ipiv[k] = p;
+        if (ck[p].re != 0.0 || ck[p].im != 0.0) {
+            if (p != k)
+                for (int64_t j = 0; j < n; ++j) {
+                    cplx t = a[j * n + k]; a[j * n + k] = a[j * n + p]; a[j * n + p] = t;
+                }
+            cplx one = {1.0, 0.0};
+            cplx rcp = cdiv(one, ck[k]);
+            for (int64_t i = k + 1; i < n; ++i) ck[i] = cmul(ck[i], rcp);
+        }
+        for (int64_t j = k + 1; j < n; ++j) {
+            cplx* cj = a + j * n;
+            cplx ukj = cj[k];
+            for (int64_t i = k + 1; i < n; ++i) cj[i] = csub(cj[i], cmul(ck[i], ukj));
+        }
+    }
+}
+
+/* b <- M^{-1} b (zgetrs: row interchanges, unit-lower then upper solve) */
+static void bdf_solve(solver_t* S, cplx* b) {
+    int64_t n = S->n;
+    const cplx* a = S->lu;
+    for (int64_t k = 0; k < n; ++k) {
+        int64_t p = S->ipiv[k];
+        if (p != k) { cplx t = b[k]; b[k] = b[p]; b[p] = t; }
+    }
+    for (int64_t k = 0; k < n; ++k) {
+        cplx bk = b[k];
+        if (bk.re == 0.0 && bk.im == 0.0) continue;
+        for (int64_t i = k + 1; i < n; ++i) b[i] = csub(b[i], cmul(bk, a[k * n + i]));
+    }
+    for (int64_t k = n - 1; k >= 0; --k) {
+        if (b[k].re == 0.0 && b[k].im == 0.0) continue;
+        b[k] = cdiv(b[k], a[k * n + k]);
+        cplx bk = b[k];
+        for (int64_t i = 0; i < k; ++i) b[i] = csub(b[i], cmul(bk, a[k * n + i]));
+    }
+}
+
+static double wrms_w2(const cplx* v, const double* w2, int64_t n) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc += (v[i].re * v[i].re + v[i].im * v[i].im) * w2[i];
+    return sqrt(acc / (double)n);
+}
+
+/* _attempt_general with the BDF corrector, ode.py:334-356, 379-423 */
+static double step_bdf(solver_t* S, int* status) {
+    const mo_problem* P = S->P;
+    int64_t n = S->n;
+    int q = S->q;
+    cplx* z = S->z;
+    const double* lvec = L(P, q);
+    const double l0 = lvec[0], conit = 0.5 / (q + 2), h = S->h;
+    const cplx* gv = (const cplx*)P->g.values;
+    for (int64_t i = 0; i < n; ++i) {
+        double w = 1.0 / (P->atol + P->rtol * cabs_(z[i]));
+        S->w2[i] = w * w;
+    }
+    memcpy(S->save, z, sizeof(cplx) * n * (q + 1));
+    for (int r = 0; r < q; ++r)
+        for (int j = q - 1; j >= r; --j)
+            for (int64_t i = 0; i < n; ++i) z[j * n + i] = cadd(z[j * n + i], z[(j + 1) * n + i]);
+    memcpy(S->ypred, z, sizeof(cplx) * n);
+    memcpy(S->z1pred, z + n, sizeof(cplx) * n);
+    int converged = 0;
+    for (int attempt = 0; attempt < 2 && !converged; ++attempt) {
+        /* _ensure_iteration_matrix */
+        const double hl0 = h * l0;
+        if (!(S->has_lu && !S->jac_stale && fabs(hl0 / S->hl0_fact - 1.0) <= 0.3)) {
+            S->jac_stale = 0;
+            bdf_factor(S, hl0);
+            S->has_lu = 1;
+            S->hl0_fact = hl0;
+            S->crate = 0.7;
+        }
+        memcpy(S->ycur, S->ypred, sizeof(cplx) * n);
+        double delp = 0.0;
+        for (int m = 0; m < MAXCOR; ++m) {
+            cplx* f = S->f;
+            for (int64_t i = 0; i < n; ++i) {
+                cplx s = {0.0, 0.0};
+                for (int64_t j = P->g.row_ptr[i]; j < P->g.row_ptr[i + 1]; ++j)
+                    s = cadd(s, cmul(gv[j], S->ycur[P->g.col_ind[j]]));
+                f[i] = s;
+            }
+            S->st[MO_STAT_NFE]++;
+            /* resid = ycur - l0 * (h f - z1pred) - ypred, left to right */
+            for (int64_t i = 0; i < n; ++i)
+                S->dy[i] = csub(csub(S->ycur[i], cscale(l0, csub(cscale(h, f[i]), S->z1pred[i]))), S->ypred[i]);
+            bdf_solve(S, S->dy);
+            for (int64_t i = 0; i < n; ++i) {
+                S->dy[i].re = -S->dy[i].re;
+                S->dy[i].im = -S->dy[i].im;
+                S->ycur[i] = cadd(S->ycur[i], S->dy[i]);
+            }
+            S->st[MO_STAT_CORR_ITERS]++;
+            double del = wrms_w2(S->dy, S->w2, n);
+            if (m > 0) {
+                double a = 0.2 * S->crate, b = del / delp;
+                S->crate = b > a ? b : a;  /* Python max(a, b) */
+            }
+            double c15 = 1.5 * S->crate;
+            if (del * (c15 < 1.0 ? c15 : 1.0) <= conit) { converged = 1; break; }
+            if (m > 0 && del > 2.0 * delp) break;
+            delp = del;
+        }
+        if (converged) break;
+        if (!S->jac_stale && attempt == 0) {
+            /* retry once with a fresh iteration matrix */
+            S->jac_stale = 1;
+            S->has_lu = 0;
+            continue;
+        }
+        break;
+    }
+    if (!converged) {
+        memcpy(z, S->save, sizeof(cplx) * n * (q + 1));
+        *status = STEP_CORRECTOR_FAIL;
+        return 0.0;
+    }
+    /* e = (ycur - ypred) / l0: numpy divides by (l0 + 0j), i.e. times 1/l0 */
+    const double rl0 = 1.0 / l0;
+    for (int64_t i = 0; i < n; ++i) S->e[i] = cscale(rl0, csub(S->ycur[i], S->ypred[i]));
+    double est = wrms_w2(S->e, S->w2, n) / P->tau2[q];
+    if (est > 1.0) {
+        memcpy(z, S->save, sizeof(cplx) * n * (q + 1));
+        *status = STEP_ERROR_REJECT;
+        return est;
+    }
+    for (int j = 0; j <= q; ++j) {
+        double lj = lvec[j];
+        for (int64_t i = 0; i < n; ++i) z[j * n + i] = cadd(z[j * n + i], cscale(lj, S->e[i]));
+    }
+    *status = STEP_OK;
+    return est;
+}
+
 static void solver_rescale(solver_t* S, double r) {
     nordsieck_rescale(S->z, S->n, S->q, r);
     S->h *= r;
@@ -331,6 +528,7 @@ static void solver_rescale(solver_t* S, double r) {
 static void solver_restart_order_one(solver_t* S, double r) {
     S->q = 1;
     S->h *= r;
+    S->has_lu = 0;
     csr_matvec(&S->P->g, S->z, S->f, S->n);
     S->st[MO_STAT_NFE]++;
     for (int64_t i = 0; i < S->n; ++i) S->z[S->n + i] = cscale(S->h, S->f[i]);
@@ -353,6 +551,8 @@ static void solver_cold_start(solver_t* S, double t0, const cplx* y0, double h0)
     S->crate = 0.7;
     S->ialth = S->q + 1;
     S->has_eprev = 0;
+    S->has_lu = 0;
+    S->jac_stale = 1;
 }
 
 static void order_step_control(solver_t* S, double est) {
@@ -401,9 +601,10 @@ static int solver_step(solver_t* S) {
         int status;
         S->st[MO_STAT_ATTEMPTS]++;
         S->st[MO_STAT_SUM_Q] += S->q;
-        double est = step_kernel(S, &status);
+        const int bdf = S->P->method == MO_METHOD_BDF;
+        double est = bdf ? step_bdf(S, &status) : step_kernel(S, &status);
         if (status == STEP_OK) {
-            cplx* tmp = S->z; S->z = S->zp; S->zp = tmp;
+            if (!bdf) { cplx* tmp = S->z; S->z = S->zp; S->zp = tmp; }
             S->t_lo = S->t;
             S->t += S->h;
             S->st[MO_STAT_STEPS]++;
@@ -426,6 +627,8 @@ static int solver_step(solver_t* S) {
         }
         S->st[MO_STAT_CORR_FAIL]++;
         ncf += 1;
+        S->jac_stale = 1;  /* ode.py:308-309 */
+        S->has_lu = 0;
         if (ncf >= 10) return MO_ERR_CORRECTOR;
         solver_rescale(S, 0.25);
     }
@@ -577,9 +780,14 @@ static void* worker(void* arg) {
     memset(&S, 0, sizeof(S));
     S.P = P;
     S.n = n;
-    cplx* mem = (cplx*)calloc((size_t)n * (2 * MO_LROWS + 7), sizeof(cplx));
+    const int bdf = P->method == MO_METHOD_BDF;
+    cplx* mem = (cplx*)calloc((size_t)n * (3 * MO_LROWS + 11) + (bdf ? (size_t)n * n : 0), sizeof(cplx));
     S.z = mem; S.zp = S.z + n * MO_LROWS; S.e = S.zp + n * MO_LROWS; S.eprev = S.e + n;
     S.ycur = S.eprev + n; S.f = S.ycur + n; S.psi = S.f + n; S.work = S.psi + n;
+    S.save = S.work + n; S.ypred = S.save + n * MO_LROWS; S.z1pred = S.ypred + n; S.dy = S.z1pred + n;
+    S.lu = S.dy + n;
+    S.ipiv = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+    S.w2 = (double*)calloc((size_t)n, sizeof(double));
     for (;;) {
         pthread_mutex_lock(&sh->mu);
         int64_t row = sh->next++;
@@ -614,12 +822,16 @@ static void* worker(void* arg) {
         }
     }
     free(mem);
+    free(S.ipiv);
+    free(S.w2);
     return NULL;
 }
 
 int mo_run(const mo_problem* P, const mo_run_args* A, mo_run_out* O) {
     if (P->dim < 1 || A->traj_end < A->traj_begin) return MO_ERR_ARGS;
     if (P->n_collapse > MO_MAX_OPS || P->n_expect > MO_MAX_OPS) return MO_ERR_ARGS;
+    if (P->method != MO_METHOD_ADAMS && P->method != MO_METHOD_BDF) return MO_ERR_ARGS;
+    if (P->method == MO_METHOD_BDF && P->max_order > MO_BDF_MAX_ORDER) return MO_ERR_ARGS;
     shared_t sh;
     sh.P = P; sh.A = A; sh.O = O; sh.next = 0; sh.first_fail = -1;
     pthread_mutex_init(&sh.mu, NULL);

@@ -7,6 +7,7 @@
 
 #define MO_LROWS 13     /* Adams max order 12 + 1 (ode.py:46, 189-190) */
 #define MO_MAX_OPS 64
+#define MO_BDF_MAX_ORDER 6 /* ode.py:46 */
 
 enum {
     MO_STREAM_PHILOX = 0,
@@ -59,7 +60,10 @@ typedef struct {
     const double* tau1;     /* [MO_LROWS] */
     const double* tau2;
     const double* tau3;
+    int32_t method;         /* 0 = ADAMS (numba kernel path), 1 = BDF (modified Newton, dense LU) */
 } mo_problem;
+
+enum { MO_METHOD_ADAMS = 0, MO_METHOD_BDF = 1 };
 
 typedef struct {
     uint64_t seed;

@@ -152,7 +152,7 @@ class DeviceProblem:
         expt = (native.QtmCsr * max(1, pk.n_expect))(*[csr(e) for e in pk.expect])
         desc = native.QtmProblemDesc(
             native.ABI_VERSION, pk.dim, csr(pk.g), pk.n_collapse, coll, pk.n_expect, expt,
-            _p(pk.psi0), pk.t_from, pk.t_to, pk.n_steps, _p(pk.times), 0, pk.rtol, pk.atol,
+            _p(pk.psi0), pk.t_from, pk.t_to, pk.n_steps, _p(pk.times), pk.method, pk.rtol, pk.atol,
             pk.max_order, pk.max_steps, pk.h0_first, _p(pk.l_table), _p(pk.tau1), _p(pk.tau2),
             _p(pk.tau3), device, variant)
         handle = C.c_void_p()

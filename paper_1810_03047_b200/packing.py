@@ -14,7 +14,7 @@ from hashlib import blake2b
 
 import numpy as np
 
-from .problem import ADAMS, adams_tables, auto_step
+from .problem import ADAMS, BDF, auto_step, method_tables
 
 __all__ = ["PackedCsr", "PackedProblem", "pack_problem"]
 
@@ -59,6 +59,7 @@ class PackedProblem:
     tau3: np.ndarray
     log_jumps: bool
     digest: int
+    method: int = 0        # 0 = ADAMS, 1 = BDF (qtm_problem_desc.method)
 
     @property
     def n_expect(self) -> int:
@@ -87,14 +88,16 @@ def _digest(parts) -> int:
 
 
 def pack_problem(problem, *, h0_first: float | None = None) -> PackedProblem:
-    """Validate and flatten.  Only the constant-generator Adams path is on
-    the device (BDF and time-dependent H(t) are "next" rows)."""
+    """Validate and flatten.  The device integrates a constant generator
+    with either method family: ADAMS (the numba kernel path,
+    _kernels.py:117-192) or BDF (modified Newton with a dense LU of
+    I - h l0 G, ode.py:334-423); the l/tau tables follow the method."""
     if getattr(problem, "generator", None) is None:
         raise ValueError("device engine needs a constant generator; the time-dependent "
                          "rhs_fn path is not on the device (SURVEY.md §8f)")
     ode = problem.ode
-    if ode.method != ADAMS:
-        raise ValueError(f"device engine implements the ADAMS path only, got {ode.method!r}")
+    if ode.method not in (ADAMS, BDF):
+        raise ValueError(f"unknown ODE method {ode.method!r}")
     g = PackedCsr.from_csr(problem.generator.g)
     psi0 = np.ascontiguousarray(np.asarray(problem.psi0, dtype=np.complex128))
     dim = psi0.shape[0]
@@ -109,17 +112,18 @@ def pack_problem(problem, *, h0_first: float | None = None) -> PackedProblem:
     if h0_first is None:
         h0_first = ode.initial_step if ode.initial_step is not None else \
             auto_step(problem.generator.g, psi0, ode.rtol, ode.atol)
-    l_tab, tau1, tau2, tau3 = adams_tables()
+    l_tab, tau1, tau2, tau3 = method_tables(ode.method)
     log_jumps = bool(getattr(getattr(problem, "options", None), "log_jumps", False))
     digest = _digest([dim, g.row_ptr, g.col_ind, g.values,
                       *[a for m in (*collapse, *expect) for a in (m.row_ptr, m.col_ind, m.values)],
                       len(collapse), len(expect), psi0, problem.t_from, problem.t_to,
                       problem.n_steps, ode.rtol, ode.atol, ode.max_order, ode.max_steps,
-                      float(h0_first)])
+                      float(h0_first)] + ([ode.method] if ode.method != ADAMS else []))
     return PackedProblem(dim=dim, g=g, collapse=collapse, expect=expect,
                          psi0=psi0.view(np.float64).copy(), t_from=float(problem.t_from),
                          t_to=float(problem.t_to), n_steps=int(problem.n_steps), times=times,
                          rtol=float(ode.rtol), atol=float(ode.atol),
                          max_order=int(ode.max_order), max_steps=int(ode.max_steps),
                          h0_first=float(h0_first), l_table=np.ascontiguousarray(l_tab.ravel()),
-                         tau1=tau1, tau2=tau2, tau3=tau3, log_jumps=log_jumps, digest=digest)
+                         tau1=tau1, tau2=tau2, tau3=tau3, log_jumps=log_jumps, digest=digest,
+                         method=0 if ode.method == ADAMS else 1)

@@ -25,8 +25,8 @@ from .csr import CsrMatrix, as_vector, csr_matvec, to_csr
 from .qops import EffectiveGenerator, OperatorSet, effective_generator
 
 __all__ = ["ADAMS", "BDF", "OdeConfig", "OdeFailure", "RunOptions", "QuantumProblem",
-           "TrajectoryResult", "average_trajectories", "adams_tables", "auto_step",
-           "LROWS"]
+           "TrajectoryResult", "average_trajectories", "adams_tables", "bdf_tables",
+           "method_tables", "auto_step", "LROWS"]
 
 ADAMS = "adams"
 BDF = "bdf"
@@ -232,6 +232,44 @@ def adams_tables(max_order: int = 12):
     for q in range(1, max_order):
         tau3[q] = tau2[q + 1]
     return l_tab, tau1, tau2, tau3
+
+
+def bdf_tables(max_order: int = 6):
+    """BDF Nordsieck vectors and error divisors (ode.py:108-119), from
+    P_q(x) = (x+1)(x+2)...(x+q) in exact rationals: l_j = [x^j]P / [x^1]P,
+    H_q = [x^1]P / [x^0]P, tau2 = (q+1) H_q (same order), tau3 = (q+2) H_q
+    (order up), tau1 = 1/(q-1)! (order down, q >= 2).  Same table layout as
+    :func:`adams_tables` (rows 7..12 unused)."""
+    l_tab = np.zeros((LROWS, LROWS))
+    tau1 = np.zeros(LROWS)
+    tau2 = np.zeros(LROWS)
+    tau3 = np.zeros(LROWS)
+    poly = [Fraction(1)]
+    for q in range(1, max_order + 1):
+        nxt = [Fraction(0)] * (len(poly) + 1)  # multiply by (x + q)
+        for i, c in enumerate(poly):
+            nxt[i] += c * q
+            nxt[i + 1] += c
+        poly = nxt
+        l_tab[q, : q + 1] = [float(c / poly[1]) for c in poly]
+        hq = poly[1] / poly[0]
+        tau2[q] = float((q + 1) * hq)
+        tau3[q] = float((q + 2) * hq)
+        if q >= 2:
+            fact = Fraction(1)
+            for i in range(2, q):
+                fact *= i
+            tau1[q] = 1.0 / float(fact)
+    return l_tab, tau1, tau2, tau3
+
+
+def method_tables(method: str):
+    """(l, tau1, tau2, tau3) of the ODE method family."""
+    if method == ADAMS:
+        return adams_tables()
+    if method == BDF:
+        return bdf_tables()
+    raise ValueError(f"unknown method {method!r}")
 
 
 def auto_step(g: CsrMatrix, y0: np.ndarray, rtol: float, atol: float) -> float:

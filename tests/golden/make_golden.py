@@ -59,6 +59,8 @@ def problem_arrays(p: QuantumProblem) -> dict:
            "initial_step": np.nan if p.ode.initial_step is None else p.ode.initial_step,
            "psi0": p.psi0, "times": p.time_grid(),
            "n_collapse": len(p.collapse_csr), "n_expect": len(p.expect_csr)}
+    if p.ode.method != "adams":
+        out["method"] = p.ode.method
     g = p.generator.g
     out.update(g_row_ptr=g.row_ptr, g_col_ind=g.col_ind, g_values=g.values)
     for tag, ops in (("c", p.collapse_csr), ("e", p.expect_csr)):
@@ -221,5 +223,41 @@ def main():
     print(f"done in {time.time() - t0:.1f}s  (mcwf {mcwf.__version__})")
 
 
+def as_bdf(p, **kw):
+    ode = OdeConfig(method="bdf", rtol=p.ode.rtol, atol=p.ode.atol, **kw)
+    return dataclasses.replace(p, ode=ode)
+
+
+def main_bdf():
+    """BDF fixtures (``bdf_*.npz``): the reference's general engine with the
+    modified-Newton corrector and scipy's LU (ode.py:334-437) on the same
+    CSR problems, plus a stiff cavity (decay rate >> drive) where BDF is the
+    method of choice."""
+    t0 = time.time()
+    plan = {"c1": (list(range(64)), list(range(16)), list(range(0, 201, 5))),
+            "c2": (list(range(16)), list(range(4)), list(range(0, 301, 10))),
+            "c3": (list(range(6)), [0], list(range(0, 501, 50)))}
+    for name, (ph, lf, pts) in plan.items():
+        p = as_bdf(ref_configs.CONFIGS[name]())
+        n_e = len(p.expect_csr)
+        save(f"bdf_{name}", p, [run_sample(p, "philox", ph, pts, n_e),
+                                run_sample(p, "lfsr113", lf, pts[:4], n_e)])
+        print(f"  bdf_{name}: {time.time() - t0:.1f}s")
+    p = as_bdf(ref_configs.stiff_cavity())
+    save("bdf_stiff", p, [run_sample(p, "philox", list(range(64)), list(range(0, 101, 10)),
+                                     len(p.expect_csr))])
+    print(f"  bdf_stiff: {time.time() - t0:.1f}s")
+    decay = QuantumProblem.from_operators(
+        OperatorSet(np.zeros((2, 2), complex), (sigma_minus(),), (sigma_z(),)),
+        fock(2, 1), 0.0, 12.0, 12, ode=OdeConfig(method="bdf", rtol=1e-8, atol=1e-12),
+        options=RunOptions(log_jumps=True))
+    save("bdf_decay_forced_jump", decay,
+         [run_sample(decay, "scripted", [0], range(13), 1, {0: [0.5, 0.3, 0.9999999]})])
+    print(f"bdf fixtures done in {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    main()
+    if "--bdf" in sys.argv:
+        main_bdf()
+    else:
+        main()

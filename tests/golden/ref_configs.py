@@ -85,4 +85,14 @@ def c5(log_jumps=True):
     return _problem(ops, fock(900, 0), 40.0, 400, log_jumps)
 
 
+def stiff_cavity(log_jumps=True):
+    """Stiff test case for the BDF fixtures (not a BASELINE config): a
+    driven cavity, N=12, whose decay rate kappa=40 far exceeds the drive
+    and detuning, t in [0, 5] with 101 output times."""
+    a = destroy(12)
+    ad = dagger(a)
+    ops = OperatorSet(0.3 * (ad @ a) + 2.0 * (a + ad), (sqrt(40.0) * a,), (ad @ a, (a + ad) / 2))
+    return _problem(ops, coherent(12, 1.0), 5.0, 100, log_jumps)
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

@@ -46,7 +46,8 @@ def load(name: str) -> Golden:
     z = dict(np.load(os.path.join(GOLDEN_DIR, f"{name}.npz"), allow_pickle=False))
     n = int(z["prob_dim"])
     init = float(z["prob_initial_step"])
-    ode = OdeConfig(rtol=float(z["prob_rtol"]), atol=float(z["prob_atol"]),
+    method = str(z["prob_method"]) if "prob_method" in z else "adams"
+    ode = OdeConfig(method=method, rtol=float(z["prob_rtol"]), atol=float(z["prob_atol"]),
                     max_order=int(z["prob_max_order"]), max_steps=int(z["prob_max_steps"]),
                     initial_step=None if np.isnan(init) else init)
     p = QuantumProblem(
@@ -71,5 +72,8 @@ CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
 SCENARIOS = ("decay_forced_jump", "decay_no_jump", "decay_streams", "rabi_closed",
              "rabi_collapse", "photon", "unitary", "trilinear")
 
+BDF_NAMES = ("bdf_c1", "bdf_c2", "bdf_c3", "bdf_stiff", "bdf_decay_forced_jump")
+
 SCRIPTS = {"decay_forced_jump": [[0.5, 0.3, 0.9999999]],
+           "bdf_decay_forced_jump": [[0.5, 0.3, 0.9999999]],
            "decay_no_jump": [[float(np.exp(-1.0) / 2)]]}

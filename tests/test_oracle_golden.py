@@ -77,3 +77,34 @@ def test_oracle_threads_do_not_change_results(oracle_lib):
     a = oracle_lib.run(pk, 5, 0, 12, n_threads=1)
     b = oracle_lib.run(pk, 5, 0, 12, n_threads=4)
     np.testing.assert_array_equal(a["values"], b["values"])
+
+
+# ---- BDF (modified Newton + dense LU, ode.py:334-423) ------------------------
+@pytest.mark.parametrize("name", goldens.BDF_NAMES)
+def test_oracle_matches_reference_bdf(name, oracle_lib):
+    g = goldens.load(name)
+    assert g.problem.ode.method == "bdf"
+    for kind in g.samples:
+        r, s = _check(name, kind, oracle_lib)
+        assert r["stats"][:, 5].sum() >= r["stats"][:, 1].sum()  # >= 1 Newton iteration per step
+
+
+def test_oracle_bdf_forced_jump_at_ln2(oracle_lib):
+    g = goldens.load("bdf_decay_forced_jump")
+    r = oracle_lib.run(pack_problem(g.problem), 0, 0, 1, stream="scripted",
+                       script=goldens.SCRIPTS["bdf_decay_forced_jump"])
+    assert r["jump_count"][0] == 1 and abs(r["jump_t"][0, 0] - np.log(2.0)) < 1e-6
+    # bit-exact on the scalar decay problem (no BLAS-ordered sums at d = 2 with one nonzero)
+    np.testing.assert_array_equal(r["values"], g.samples["scripted"].values)
+
+
+def test_bdf_tables_match_generating_polynomials():
+    from paper_1810_03047_b200.problem import bdf_tables
+    l, t1, t2, t3 = bdf_tables()
+    # q = 1: backward Euler, l = [1, 1], error constant 2 (ode.py:108-119)
+    np.testing.assert_array_equal(l[1, :2], [1.0, 1.0])
+    assert t2[1] == 2.0 and t3[1] == 3.0
+    # q = 2: P = (x+1)(x+2) = 2 + 3x + x^2 -> l = [2/3, 1, 1/3], H_2 = 3/2
+    np.testing.assert_allclose(l[2, :3], [2 / 3, 1.0, 1 / 3], rtol=0, atol=0)
+    assert t2[2] == 4.5 and t1[2] == 1.0
+    assert np.all(l[7:] == 0.0)
