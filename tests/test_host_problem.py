@@ -100,11 +100,20 @@ def test_problem_validation_mirrors_reference():
         OdeConfig(max_order=13)
 
 
-def test_pack_rejects_paths_outside_the_device():
+def test_pack_selects_method_tables():
     p = QuantumProblem.from_operators(OperatorSet(sigma_x(), (), (sigma_z(),)), fock(2, 0),
                                       0.0, 1.0, 10, ode=OdeConfig(method=BDF))
-    with pytest.raises(ValueError, match="ADAMS"):
-        pack_problem(p)
+    pk = pack_problem(p)
+    assert pk.method == 1 and pk.max_order == 6
+    assert pk.tau2[2] == 4.5 and pk.tau1[2] == 1.0  # BDF2 divisors (Adams2: tau2 = 12)
+    assert pk.l_table[2 * 13 + 0] == 2.0 / 3.0  # BDF2 l0 = 2/3 (Adams2: 1/2)
+    pa = pack_problem(QuantumProblem.from_operators(
+        OperatorSet(sigma_x(), (), (sigma_z(),)), fock(2, 0), 0.0, 1.0, 10))
+    assert pa.method == 0 and pa.l_table[2 * 13 + 0] == 0.5
+    assert pa.digest != pk.digest
+
+
+def test_pack_rejects_paths_outside_the_device():
     p2 = QuantumProblem(generator=None, collapse_csr=(), expect_csr=(), psi0=fock(2, 0),
                         t_from=0.0, t_to=1.0, n_steps=10, rhs_fn=lambda t, y: y)
     with pytest.raises(ValueError, match="rhs_fn"):
