@@ -1,0 +1,596 @@
+// qtm_bdf.cuh -- persistent sm_100a kernel for the BDF method family:
+// quantum trajectories integrated with the reference's general engine,
+// BDF orders 1-6 with the modified-Newton corrector on the iteration matrix
+// M = I - h l0 G (G = the constant CSR generator, i.e. the Jacobian).
+//
+// Reference behaviour reproduced (see oracle/mcwf_oracle.c for the CPU
+// restatement this kernel is checked against):
+//   _attempt_general: weights, save, predict, Newton, error test,
+//     commit or restore .................................... ode.py:334-356
+//   _newton_correct: <= 3 iterations, resid = y - l0 (h G y - z1) - ypred,
+//     dy = -M^{-1} resid, one retry with a fresh matrix ..... ode.py:379-407
+//   _ensure_iteration_matrix: refactor when there is no LU, the Jacobian is
+//     stale, or |h l0 / h l0_fact - 1| > 0.3; crate = 0.7 .. ode.py:409-423
+//   scipy lu_factor / lu_solve (LAPACK zgetrf / zgetrs): unblocked
+//     right-looking LU with partial pivoting (izamax: first row of maximal
+//     |re| + |im|), reciprocal scaling of the sub-column, rank-1 update;
+//     row interchanges, unit-lower and upper column-oriented solves
+//   step retry loop, order/step control, jumps, recording: as the Adams
+//     kernel (ode.py:261-329, 441-466; trajectory.py:133-250)
+//
+// Mapping.  One CTA per trajectory at a time (persistent, atomic work
+// counter), NT threads own components i = tid + NT*k.  Every vector of the
+// trajectory -- 7 Nordsieck rows, their saved copy, the Newton vectors --
+// and the LU of M live in one per-CTA workspace: dynamic shared memory when
+// it fits (d <= ~100), otherwise a per-CTA slice of HBM (L2-resident for
+// moderate d).  The LU factorisation and the triangular solves are
+// sequential in the pivot index, so they run as CTA-wide sweeps with one
+// barrier per pivot; the trailing update walks columns by warp and rows by
+// lane (column-major storage: coalesced, conflict-free).  There are no
+// reductions inside the LU or the solves, so with -fmad=false they are
+// bit-identical to the oracle's restatement.
+#pragma once
+#include "qtm_traj.cuh"
+
+namespace qtm {
+
+constexpr int BDF_ROWS = 7;  // BDF order <= 6 (ode.py:46): rows 0..6
+
+struct BdfParams {
+    double2* ws;             // per-CTA workspaces in HBM (when not in shared memory)
+    long long ws_stride;     // double2 elements per CTA workspace
+    int in_smem;             // 1: the workspace is the kernel's dynamic shared memory
+};
+
+// workspace layout in double2 units (d = state dimension)
+struct BdfLayout {
+    long long z, save, ypred, z1p, ycur, dy, x, e0, e1, psi, w2, ipiv, lu, total;
+    __host__ __device__ static BdfLayout make(long long d) {
+        BdfLayout L{};
+        long long o = 0;
+        L.z = o;     o += BDF_ROWS * d;
+        L.save = o;  o += BDF_ROWS * d;
+        L.ypred = o; o += d;
+        L.z1p = o;   o += d;
+        L.ycur = o;  o += d;
+        L.dy = o;    o += d;
+        L.x = o;     o += d;
+        L.e0 = o;    o += d;
+        L.e1 = o;    o += d;
+        L.psi = o;   o += d;
+        L.w2 = o;    o += (d + 1) / 2;   // doubles
+        L.ipiv = o;  o += (d + 3) / 4;   // ints
+        L.lu = o;    o += d * d;         // column-major: A(i, j) at lu[j*d + i]
+        L.total = o;
+        return L;
+    }
+};
+
+// a / b in numpy's order (Smith's algorithm, npymath complex divide)
+__device__ __forceinline__ double2 cdiv_np(double2 a, double2 b) {
+    const double abr = fabs(b.x), abi = fabs(b.y);
+    if (abr >= abi) {
+        if (abr == 0.0 && abi == 0.0) return make_double2(a.x / abr, a.y / abr);
+        const double rat = b.y / b.x, scl = 1.0 / (b.x + b.y * rat);
+        return make_double2((a.x + a.y * rat) * scl, (a.y - a.x * rat) * scl);
+    }
+    const double rat = b.x / b.y, scl = 1.0 / (b.y + b.x * rat);
+    return make_double2((a.x * rat + a.y) * scl, (a.y * rat - a.x) * scl);
+}
+
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// M = I - hl0 G from the CSR generator, factored in place (zgetf2 order)
+template <int NT>
+__device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
+                           double hl0, double* s_pv, int* s_pi) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = P.d;
+    const long long dd = (long long)d * d;
+    for (long long k = tid; k < dd; k += NT) A[k] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int i = tid; i < d; i += NT) {
+        const int b = __ldg(P.g.rp + i), en = __ldg(P.g.rp + i + 1);
+        for (int j = b; j < en; ++j) {
+            const double2 v = __ldg(P.g.v + j);
+            A[(long long)__ldg(P.g.ci + j) * d + i] = make_double2(-hl0 * v.x, -hl0 * v.y);
+        }
+        A[(long long)i * d + i].x += 1.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < d; ++k) {
+        double2* const ck = A + (long long)k * d;
+        // izamax over rows k..d-1: the first row of maximal |re| + |im|
+        double bv = -1.0;
+        int bi = d;
+        for (int i = k + tid; i < d; i += NT) {
+            const double2 a = ck[i];
+            const double v = fabs(a.x) + fabs(a.y);
+            if (v > bv) { bv = v; bi = i; }
+        }
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, m);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        if constexpr (NW > 1) {
+            if (lane == 0) { s_pv[warp] = bv; s_pi[warp] = bi; }
+            __syncthreads();
+            bv = s_pv[0];
+            bi = s_pi[0];
+            for (int w = 1; w < NW; ++w)
+                if (s_pv[w] > bv || (s_pv[w] == bv && s_pi[w] < bi)) { bv = s_pv[w]; bi = s_pi[w]; }
+        }
+        const int p = bi < d ? bi : k;
+        if (tid == 0) ipiv[k] = p;
+        const double2 piv = ck[p];
+        __syncthreads();  // every thread holds the pivot before the rows move
+        if (piv.x != 0.0 || piv.y != 0.0) {
+            if (p != k) {
+                for (int j = tid; j < d; j += NT) {
+                    double2* const cj = A + (long long)j * d;
+                    const double2 t = cj[k];
+                    cj[k] = cj[p];
+                    cj[p] = t;
+                }
+            }
+            const double2 rcp = cdiv_np(make_double2(1.0, 0.0), piv);
+            __syncthreads();
+            for (int i = k + 1 + tid; i < d; i += NT) ck[i] = cmul2(ck[i], rcp);
+        }
+        __syncthreads();
+        // trailing update: A(i, j) -= L(i, k) U(k, j), columns by warp, rows by lane
+        for (int j = k + 1 + warp; j < d; j += NW) {
+            double2* const cj = A + (long long)j * d;
+            const double2 ukj = cj[k];
+            for (int i = k + 1 + lane; i < d; i += 32) {
+                const double2 l = ck[i];
+                const double2 a = cj[i];
+                cj[i] = make_double2(a.x - (l.x * ukj.x - l.y * ukj.y), a.y - (l.x * ukj.y + l.y * ukj.x));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// x = M^{-1} b (zgetrs): b is overwritten (interchanges + forward sweep)
+template <int NT>
+__device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __restrict__ ipiv,
+                          double2* __restrict__ b, double2* __restrict__ x) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k < d; ++k) {
+            const int p = ipiv[k];
+            if (p != k) { const double2 t = b[k]; b[k] = b[p]; b[p] = t; }
+        }
+    }
+    __syncthreads();
+    for (int k = 0; k < d; ++k) {
+        const double2 bk = b[k];
+        if (bk.x == 0.0 && bk.y == 0.0) continue;
+        const double2* const ck = A + (long long)k * d;
+        for (int i = k + 1 + tid; i < d; i += NT) {
+            const double2 a = ck[i], bi = b[i];
+            b[i] = make_double2(bi.x - (bk.x * a.x - bk.y * a.y), bi.y - (bk.x * a.y + bk.y * a.x));
+        }
+        __syncthreads();
+    }
+    for (int k = d - 1; k >= 0; --k) {
+        double2 xk = b[k];
+        if (xk.x != 0.0 || xk.y != 0.0) {
+            const double2* const ck = A + (long long)k * d;
+            xk = cdiv_np(xk, ck[k]);
+            for (int i = tid; i < k; i += NT) {
+                const double2 a = ck[i], bi = b[i];
+                b[i] = make_double2(bi.x - (xk.x * a.x - xk.y * a.y), bi.y - (xk.x * a.y + xk.y * a.x));
+            }
+        }
+        if (tid == 0) x[k] = xk;
+        __syncthreads();
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ double bsum1(double v, double* red, int& phase) {
+    double a[1] = {v};
+    block_sum<NT, 1>(a, red, phase);
+    return a[0];
+}
+
+// Horner of the history polynomial at s for component i (nordsieck_eval)
+__device__ __forceinline__ double2 bdf_horner(const double2* Z, int d, int q, double s, int i) {
+    double2 acc = Z[(long long)q * d + i];
+    for (int j = q - 1; j >= 0; --j) acc = cadd(cscale(s, acc), Z[(long long)j * d + i]);
+    return acc;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R,
+           const __grid_constant__ BdfParams B) {
+    constexpr int NW = NT / 32;
+    extern __shared__ double2 smem[];
+    __shared__ double red[2 * KRED * (NW > 1 ? NW : 1)];
+    __shared__ double s_pv[NW];
+    __shared__ int s_pi[NW];
+    __shared__ long long s_row;
+    __shared__ Stream s_stream;
+    __shared__ double s_draw;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int d = P.d, npts = P.n_pts;
+    const BdfLayout L = BdfLayout::make(d);
+    double2* const ws = B.in_smem ? smem : B.ws + (long long)blockIdx.x * B.ws_stride;
+    double2* const Z = ws + L.z;
+    double2* const SV = ws + L.save;
+    double2* const YP = ws + L.ypred;
+    double2* const Z1 = ws + L.z1p;
+    double2* const YC = ws + L.ycur;
+    double2* const DY = ws + L.dy;
+    double2* const X = ws + L.x;
+    double2* const PS = ws + L.psi;
+    double* const W2 = reinterpret_cast<double*>(ws + L.w2);
+    int* const IPIV = reinterpret_cast<int*>(ws + L.ipiv);
+    double2* const A = ws + L.lu;
+    int rphase = 0;
+
+    for (;;) {
+        if (tid == 0) s_row = (long long)atomicAdd(R.counter, 1ull);
+        __syncthreads();
+        const long long row = s_row;
+        if (row >= R.n_traj) break;
+        if (tid == 0)
+            s_stream.init(R.stream_kind, R.seed, (uint64_t)(R.traj_begin + row),
+                          R.script ? R.script + row * R.script_stride : nullptr,
+                          R.script_len ? R.script_len[row] : 0, R.script_fallback);
+        __syncthreads();
+
+        long long st[NSTATS];
+#pragma unroll
+        for (int s = 0; s < NSTATS; ++s) st[s] = 0;
+        int rc = kOk;
+        double err0 = 0.0, err1 = 0.0, err2 = 0.0, err3 = 0.0;
+        long long njumps = 0, steps_in_segment = 0;
+        double t = P.t_from, h = P.h0_first, t_lo = P.t_from, crate = 0.7, hl0_fact = 1.0, r_thr = 0.0;
+        int q = 1, ialth = 2, gi = 1, ecur = 0;
+        bool has_eprev = false, has_lu = false, jac_stale = true;
+
+        // one uniform draw (thread 0 evaluates, broadcast)
+        auto draw = [&]() -> double {
+            __syncthreads();
+            if (tid == 0) s_draw = s_stream.next();
+            __syncthreads();
+            return s_draw;
+        };
+        // per-warp partial sums of <psi|E_k|psi> and <psi|psi> (PS complete)
+        auto record = [&](int g) {
+            __syncthreads();
+            double* const rp = R.rec_partial + ((size_t)row * npts + g) * (size_t)(P.ne + 1) * NW + (tid >> 5);
+            for (int k = 0; k <= P.ne; ++k) {
+                double acc[1] = {0.0};
+                for (int i = tid; i < d; i += NT) {
+                    const double2 p = PS[i];
+                    if (k < P.ne) {
+                        const double2 s = row_dot(P.e[k], i, PS);
+                        acc[0] += p.x * s.x - (-p.y) * s.y;
+                    } else {
+                        acc[0] += cabs2(p);
+                    }
+                }
+                warp_sum_lane0<1>(acc);
+                if (lane == 0) rp[(size_t)k * NW] = acc[0];
+            }
+        };
+        // psi at grid point g (Horner at the current step), then record
+        auto record_grid = [&](int g) {
+            const double s = (P.times[g] - t) / h;
+            __syncthreads();
+            for (int i = tid; i < d; i += NT) PS[i] = bdf_horner(Z, d, q, s, i);
+            record(g);
+        };
+        // new solver at (t0, y0 in vector Y) with step h0 (ode.py:164-217)
+        auto cold_start = [&](double t0, const double2* Y, double h0) {
+            t = t0; t_lo = t0; q = 1; h = h0;
+            __syncthreads();
+            for (int i = tid; i < d; i += NT) {
+                const double2 f = row_dot(P.g, i, Y);
+                Z[i] = Y[i];
+                Z[(long long)d + i] = cscale(h, f);
+            }
+            st[sNfe]++;
+            crate = 0.7; ialth = 2; has_eprev = false; has_lu = false; jac_stale = true;
+            __syncthreads();
+        };
+        auto rescale = [&](double r) {
+            double f = 1.0;
+            for (int j = 1; j <= q; ++j) {
+                f *= r;
+                for (int i = tid; i < d; i += NT) Z[(long long)j * d + i] = cscale(f, Z[(long long)j * d + i]);
+            }
+            h *= r;
+            has_eprev = false;
+            ialth = q + 1;
+        };
+
+        for (int i = tid; i < d; i += NT) PS[i] = P.psi0[i];
+        record(0);
+        r_thr = draw();
+        for (int i = tid; i < d; i += NT) YC[i] = P.psi0[i];
+        cold_start(P.t_from, YC, P.h0_first);
+
+        while (gi < npts) {
+            // ================= OdeSolver.step() (ode.py:261-312) =================
+            int nef = 0, ncf = 0;
+            double est = 0.0;
+            for (;;) {
+                if (t + h == t) { rc = kErrStepCollapse; err0 = t; err1 = h; goto traj_done; }
+                st[sAttempts]++;
+                st[sSumQ] += q;
+                const double* const lv = P.l[q];
+                const double l0 = lv[0], conit = P.conit[q];
+                // weights, save, predict (ode.py:336-342)
+                for (int i = tid; i < d; i += NT) {
+                    const double2 z0 = Z[i];
+                    const double w = 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y));
+                    W2[i] = w * w;
+                    for (int j = 0; j <= q; ++j) SV[(long long)j * d + i] = Z[(long long)j * d + i];
+                    for (int r = 0; r < q; ++r)
+                        for (int j = q - 1; j >= r; --j)
+                            Z[(long long)j * d + i] = cadd(Z[(long long)j * d + i], Z[(long long)(j + 1) * d + i]);
+                    YP[i] = Z[i];
+                    Z1[i] = Z[(long long)d + i];
+                }
+                bool converged = false;
+                for (int attempt = 0; attempt < 2 && !converged; ++attempt) {
+                    // _ensure_iteration_matrix (ode.py:409-423)
+                    const double hl0 = h * l0;
+                    if (!(has_lu && !jac_stale && fabs(hl0 / hl0_fact - 1.0) <= 0.3)) {
+                        jac_stale = false;
+                        bdf_factor<NT>(P, A, IPIV, hl0, s_pv, s_pi);
+                        has_lu = true;
+                        hl0_fact = hl0;
+                        crate = 0.7;
+                    }
+                    for (int i = tid; i < d; i += NT) YC[i] = YP[i];
+                    __syncthreads();
+                    double delp = 0.0;
+                    for (int m = 0; m < 3; ++m) {
+                        // resid = ycur - l0 * (h G ycur - z1pred) - ypred (left to right)
+                        for (int i = tid; i < d; i += NT) {
+                            const double2 f = row_dot(P.g, i, YC);
+                            DY[i] = csub(csub(YC[i], cscale(l0, csub(cscale(h, f), Z1[i]))), YP[i]);
+                        }
+                        st[sNfe]++;
+                        bdf_solve<NT>(d, A, IPIV, DY, X);
+                        double acc = 0.0;
+                        for (int i = tid; i < d; i += NT) {
+                            const double2 xi = X[i];
+                            const double2 dy = make_double2(-xi.x, -xi.y);
+                            YC[i] = cadd(YC[i], dy);
+                            acc += cabs2(dy) * W2[i];
+                        }
+                        st[sCorrIters]++;
+                        const double del = sqrt(bsum1<NT>(acc, red, rphase) / (double)d);
+                        if (m > 0) {
+                            const double a = 0.2 * crate, b = del / delp;
+                            crate = b > a ? b : a;  // Python max(a, b)
+                        }
+                        const double c15 = 1.5 * crate;
+                        if (del * (c15 < 1.0 ? c15 : 1.0) <= conit) { converged = true; break; }
+                        if (m > 0 && del > 2.0 * delp) break;
+                        delp = del;
+                    }
+                    if (converged) break;
+                    if (!jac_stale && attempt == 0) {  // retry once with a fresh matrix
+                        jac_stale = true;
+                        has_lu = false;
+                        continue;
+                    }
+                    break;
+                }
+                if (converged) {
+                    // e = (ycur - ypred) / l0: numpy divides by (l0 + 0j) = times 1/l0
+                    const double rl0 = 1.0 / l0;
+                    double2* const ec = ws + (ecur ? L.e1 : L.e0);
+                    double acc = 0.0;
+                    for (int i = tid; i < d; i += NT) {
+                        const double2 e = cscale(rl0, csub(YC[i], YP[i]));
+                        ec[i] = e;
+                        acc += cabs2(e) * W2[i];
+                    }
+                    est = sqrt(bsum1<NT>(acc, red, rphase) / (double)d) / P.tau2[q];
+                    if (!(est > 1.0)) {
+                        for (int i = tid; i < d; i += NT) {
+                            const double2 e = ec[i];
+                            for (int j = 0; j <= q; ++j)
+                                Z[(long long)j * d + i] = cadd(Z[(long long)j * d + i], cscale(lv[j], e));
+                        }
+                        break;  // accepted
+                    }
+                }
+                // rejected: restore the saved history (ode.py:346, 350)
+                for (int i = tid; i < d; i += NT)
+                    for (int j = 0; j <= q; ++j) Z[(long long)j * d + i] = SV[(long long)j * d + i];
+                if (!converged) {
+                    st[sCorrFail]++;
+                    ncf++;
+                    jac_stale = true;  // ode.py:308-309
+                    has_lu = false;
+                    if (ncf >= 10) { rc = kErrCorrector; err0 = t; err1 = h; goto traj_done; }
+                    rescale(0.25);
+                    continue;
+                }
+                st[sErrReject]++;
+                if (++nef >= 10) { rc = kErrRepeatedErrTest; err0 = t; err1 = h; goto traj_done; }
+                if (nef >= 3) {
+                    // _restart_order_one(0.1), ode.py:314-323
+                    q = 1;
+                    h *= 0.1;
+                    __syncthreads();
+                    for (int i = tid; i < d; i += NT) X[i] = Z[i];
+                    __syncthreads();
+                    for (int i = tid; i < d; i += NT) Z[(long long)d + i] = cscale(h, row_dot(P.g, i, X));
+                    st[sNfe]++;
+                    has_eprev = false;
+                    ialth = q + 1;
+                    has_lu = false;
+                } else {
+                    const double rr = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
+                    const double m1 = 0.9 < rr ? 0.9 : rr;
+                    rescale(m1 > 0.1 ? m1 : 0.1);
+                }
+            }
+            // accepted step bookkeeping (ode.py:281-292)
+            t_lo = t;
+            t += h;
+            st[sSteps]++;
+            if (--ialth == 0) {
+                // _order_step_control (ode.py:441-466); weights from the new z0
+                const bool need_d = q > 1, need_u = q < P.max_order && has_eprev;
+                double v[2] = {0.0, 0.0};
+                const double2* const ecp = ws + (ecur ? L.e1 : L.e0);
+                const double2* const epp = ws + (ecur ? L.e0 : L.e1);
+                for (int i = tid; i < d; i += NT) {
+                    const double2 z0 = Z[i];
+                    const double w = 1.0 / (P.atol + P.rtol * hypot(z0.x, z0.y));
+                    const double2 zq = Z[(long long)q * d + i];
+                    const double2 de = csub(ecp[i], epp[i]);
+                    v[0] += cabs2(zq) * w * w;
+                    v[1] += cabs2(de) * w * w;
+                }
+                block_sum<NT, 2>(v, red, rphase);
+                const double r_same = 1.0 / (1.2 * pow(est, P.rq1[q]) + 1e-6);
+                double r_down = 0.0, r_up = 0.0;
+                if (need_d) r_down = 1.0 / (1.3 * pow(sqrt(v[0] / (double)d) / P.tau1[q], P.rq0[q]) + 1e-6);
+                if (need_u) r_up = 1.0 / (1.4 * pow(sqrt(v[1] / (double)d) / P.tau3[q], P.rq2[q]) + 1e-6);
+                double best = r_same;
+                if (r_down > best) best = r_down;
+                if (r_up > best) best = r_up;
+                if (best < 1.1) {
+                    ialth = 3;
+                    ecur ^= 1;  // e_prev = e
+                    has_eprev = true;
+                } else {
+                    if (best == r_up) {
+                        const double cu = P.l[q][q] / (q + 1);
+                        for (int i = tid; i < d; i += NT) Z[(long long)(q + 1) * d + i] = cscale(cu, ecp[i]);
+                        q = q + 1;
+                        st[sOrderUp]++;
+                    } else if (best == r_down) {
+                        q = q - 1;
+                        st[sOrderDown]++;
+                    }
+                    const double m1 = 10.0 < best ? 10.0 : best;
+                    rescale(m1 > 0.1 ? m1 : 0.1);
+                }
+            } else {
+                ecur ^= 1;  // e_prev = e
+                has_eprev = true;
+            }
+            // ================= trajectory loop body (trajectory.py:225-246) =======
+            if (++steps_in_segment > P.max_steps) { rc = kErrMaxSteps; err0 = t; err1 = h; goto traj_done; }
+            if (P.nc > 0) {
+                double nrm = 0.0;
+                for (int i = tid; i < d; i += NT) nrm += cabs2(Z[i]);
+                nrm = bsum1<NT>(nrm, red, rphase);
+                if (nrm < r_thr) {
+                    // locate_jump_time (trajectory.py:157-182)
+                    double v2[2] = {0.0, 0.0};
+                    const double s_lo = (t_lo - t) / h, s_hi = (t - t) / h;
+                    for (int i = tid; i < d; i += NT) {
+                        v2[0] += cabs2(bdf_horner(Z, d, q, s_lo, i));
+                        v2[1] += cabs2(bdf_horner(Z, d, q, s_hi, i));
+                    }
+                    block_sum<NT, 2>(v2, red, rphase);
+                    const double f_lo = v2[0], f_hi = v2[1];
+                    const double tol = 1e-9 * r_thr;
+                    if (f_lo < r_thr - tol || f_hi > r_thr + tol) {
+                        rc = kErrBracket; err0 = t_lo; err1 = t; err2 = f_lo; err3 = f_hi;
+                        goto traj_done;
+                    }
+                    double ts;
+                    if (f_lo <= r_thr + tol) {
+                        ts = t_lo;
+                    } else {
+                        double a = t_lo, b = t;
+                        bool found = false;
+                        ts = 0.0;
+                        for (int it = 0; it < 60; ++it) {
+                            const double mid = 0.5 * (a + b);
+                            const double sm = (mid - t) / h;
+                            double acc = 0.0;
+                            for (int i = tid; i < d; i += NT) acc += cabs2(bdf_horner(Z, d, q, sm, i));
+                            const double fm = bsum1<NT>(acc, red, rphase);
+                            st[sBisect]++;
+                            if (fabs(fm - r_thr) <= tol) { ts = mid; found = true; break; }
+                            if (fm > r_thr) a = mid; else b = mid;
+                        }
+                        if (!found) ts = 0.5 * (a + b);
+                    }
+                    if (ts <= P.t_to) {
+                        while (gi < npts && P.times[gi] <= ts) { record_grid(gi); gi++; }
+                        // psi(t*) and the collapse (trajectory.py:235-241, 133-154)
+                        const double sst = (ts - t) / h;
+                        __syncthreads();
+                        for (int i = tid; i < d; i += NT) PS[i] = bdf_horner(Z, d, q, sst, i);
+                        const double u = draw();  // (draw() synchronises: PS complete)
+                        double wts[MAXOPS];
+                        for (int c0 = 0; c0 < P.nc; c0 += KRED) {
+                            double v4[KRED] = {0.0, 0.0, 0.0, 0.0};
+                            for (int kk = 0; kk < KRED; ++kk)
+                                if (c0 + kk < P.nc)
+                                    for (int i = tid; i < d; i += NT) v4[kk] += cabs2(row_dot(P.c[c0 + kk], i, PS));
+                            block_sum<NT, KRED>(v4, red, rphase);
+                            for (int kk = 0; kk < KRED; ++kk) if (c0 + kk < P.nc) wts[c0 + kk] = v4[kk];
+                        }
+                        double dp = 0.0;
+                        for (int c = 0; c < P.nc; ++c) dp += wts[c];
+                        if (dp <= 0.0) { rc = kErrNoSupport; err0 = t; err1 = h; goto traj_done; }
+                        int idx = 0;
+                        for (int c = 0; c < P.nc; ++c) if (wts[c] > 0.0) idx = c;
+                        double cum = 0.0;
+                        for (int c = 0; c < P.nc; ++c) {
+                            cum += wts[c] / dp;
+                            if (wts[c] > 0.0 && cum >= u) { idx = c; break; }
+                        }
+                        const double scl = 1.0 / sqrt(wts[idx]);
+                        for (int i = tid; i < d; i += NT) YC[i] = cscale(scl, row_dot(P.c[idx], i, PS));
+                        if (tid == 0 && njumps < R.max_jumps) {
+                            R.jump_t[(size_t)row * R.max_jumps + njumps] = ts;
+                            R.jump_idx[(size_t)row * R.max_jumps + njumps] = idx;
+                        }
+                        njumps++;
+                        st[sJumps]++;
+                        r_thr = draw();
+                        cold_start(ts, YC, h);
+                        steps_in_segment = 0;
+                        continue;
+                    }
+                }
+            }
+            while (gi < npts && P.times[gi] <= t) { record_grid(gi); gi++; }
+        }
+    traj_done:
+        if (tid == 0) {
+            st[sDraws] = (long long)s_stream.n;
+            long long* so = R.stats + (size_t)row * NSTATS;
+            for (int s = 0; s < NSTATS; ++s) so[s] = st[s];
+            R.status[row] = rc;
+            R.jump_count[row] = njumps;
+            if (rc != kOk) {
+                double* eo = R.err + (size_t)row * 4;
+                eo[0] = err0; eo[1] = err1; eo[2] = err2; eo[3] = err3;
+                if (rc == kErrBracket) R.err_r[row] = r_thr;
+                atomicMin(R.first_fail, (unsigned long long)row);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace qtm

@@ -20,6 +20,7 @@
 
 #include "../../include/qtm.h"
 #include "qtm_traj.cuh"
+#include "qtm_bdf.cuh"
 
 using namespace qtm;
 
@@ -210,6 +211,13 @@ struct qtm_problem {
     DevBuf<int> status, jump_idx;
     DevBuf<double2> zovf;
     DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row, [2..17] phases
+    // BDF method (qtm_bdf.cuh): kernel, block size, workspace placement
+    int method = 0;
+    const void* bdf_fn = nullptr;
+    int bdf_threads = 0;
+    bool bdf_in_smem = false;
+    long long bdf_ws_elems = 0;  // double2 per CTA workspace
+    DevBuf<double2> bdf_ws;
     std::mutex mu;
 };
 
@@ -453,6 +461,7 @@ void free_problem(qtm_problem* p) {
     p->sum.release(s); p->sumsq.release(s); p->jump_t.release(s); p->script.release(s);
     p->stats.release(s); p->jump_count.release(s); p->script_len.release(s); p->stats_tot.release(s);
     p->status.release(s); p->jump_idx.release(s); p->zovf.release(s); p->ctl.release(s);
+    p->bdf_ws.release(s);
     if (s) cudaStreamSynchronize(s);
     for (auto& e : p->ev) if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
@@ -487,18 +496,21 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     *out = nullptr;
     if (d->abi_version != QTM_ABI_VERSION) return set_error(QTM_ERR_ARGS, "ABI version mismatch");
     if (d->dim < 1) return set_error(QTM_ERR_ARGS, "dim must be positive");
-    if (d->method != 0) return set_error(QTM_ERR_UNSUPPORTED, "only the ADAMS method is implemented on the device");
+    if (d->method != 0 && d->method != 1) return set_error(QTM_ERR_ARGS, "method must be 0 (ADAMS) or 1 (BDF)");
+    if (d->method == 1 && d->max_order > BDF_ROWS - 1) return set_error(QTM_ERR_ARGS, "max_order must be in [1, 6] for BDF");
+    if (d->method == 1 && d->dim > 8192) return set_error(QTM_ERR_UNSUPPORTED, "BDF: dense LU of I - h l0 G limited to dim <= 8192");
     if (d->n_collapse < 0 || d->n_collapse > QTM_MAX_OPS || d->n_expect < 0 || d->n_expect > QTM_MAX_OPS)
         return set_error(QTM_ERR_UNSUPPORTED, "at most 32 collapse and 32 expectation operators");
     if (d->max_order < 1 || d->max_order > 12) return set_error(QTM_ERR_ARGS, "max_order must be in [1, 12]");
     if (d->n_steps < 1 || !d->times || !d->psi0) return set_error(QTM_ERR_ARGS, "grid / psi0 missing");
     if (!(d->h0_first > 0.0)) return set_error(QTM_ERR_ARGS, "h0_first must be positive");
     if (!d->l_table || !d->tau1 || !d->tau2 || !d->tau3) return set_error(QTM_ERR_ARGS, "Adams tables missing");
-    int variant = d->variant >= 0 ? d->variant : auto_variant(d->dim);
+    // (BDF runs its own kernel, qtm_bdf.cuh; the Adams variant slot is unused)
+    int variant = d->method == 1 ? 0 : (d->variant >= 0 ? d->variant : auto_variant(d->dim));
     if (variant < 0 || variant >= (int)variants().size())
         return set_error(QTM_ERR_UNSUPPORTED, "no kernel variant for this dimension");
     const Variant& var = variants()[variant];
-    if ((int64_t)var.threads * var.comps < d->dim)
+    if (d->method == 0 && (int64_t)var.threads * var.comps < d->dim)
         return set_error(QTM_ERR_ARGS, "kernel variant too small for this dimension");
 
     qtm_problem* p = new qtm_problem();
@@ -508,6 +520,7 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     p->n_expect = d->n_expect;
     p->n_collapse = d->n_collapse;
     p->n_pts = d->n_steps + 1;
+    p->method = d->method;
     cudaError_t ce = cudaSetDevice(d->device);
     if (ce != cudaSuccess) {
         delete p;
@@ -578,11 +591,29 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (rc == QTM_OK &&
         cudaFuncSetAttribute(var.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_cap) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem) failed");
-    if (rc == QTM_OK) {
+    if (rc == QTM_OK && p->method == 1) {
+        // BDF: one kernel per block size; the per-trajectory workspace (history,
+        // Newton vectors, LU of the iteration matrix) goes to shared memory when
+        // it fits, else to a per-CTA slice of HBM
+        p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
+        p->bdf_fn = p->bdf_threads == 32 ? (const void*)bdf_kernel<32>
+                    : p->bdf_threads == 128 ? (const void*)bdf_kernel<128> : (const void*)bdf_kernel<256>;
+        p->bdf_ws_elems = BdfLayout::make(d->dim).total;
+        cudaFuncAttributes battr;
+        size_t bstatic = 4096;
+        if (cudaFuncGetAttributes(&battr, p->bdf_fn) == cudaSuccess) bstatic = battr.sharedSizeBytes;
+        const size_t bcap = (size_t)smem_cap > bstatic ? (size_t)smem_cap - bstatic : 0;
+        const size_t bytes = sizeof(double2) * (size_t)p->bdf_ws_elems;
+        p->bdf_in_smem = bytes <= bcap;
+        p->smem = p->bdf_in_smem ? bytes : 0;
+        if (cudaFuncSetAttribute(p->bdf_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bcap) != cudaSuccess)
+            rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem, BDF) failed");
+    }
+    if (rc == QTM_OK && p->method == 0) {
         bool staged = false;
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged);
     }
-    if (rc == QTM_OK) rc = build_expect_diag(p, d, var.threads * var.comps);
+    if (rc == QTM_OK && p->method == 0) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
     if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "problem upload failed");
@@ -602,7 +633,10 @@ int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
     int sms = 0, per_sm = 0;
     CUDA_TRY(cudaSetDevice(p->device));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
+    if (p->method == 1)
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->bdf_fn, p->bdf_threads, p->smem));
+    else
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
     *ctas = sms * per_sm;
     return QTM_OK;
 }
@@ -612,6 +646,10 @@ int qtm_problem_layout(qtm_problem* p, int32_t* reg_rows, int32_t* smem_rows, in
     const Variant& var = variants()[p->variant];
     *reg_rows = var.reg_rows > 0 ? std::min(var.reg_rows, LROWS) : 0;
     *smem_rows = var.reg_rows > 0 ? 0 : LROWS;
+    if (p->method == 1) {  // BDF: the whole workspace in shared memory or in HBM
+        *reg_rows = 0;
+        *smem_rows = p->bdf_in_smem ? BDF_ROWS : 0;
+    }
     *smem_bytes = (int64_t)p->smem;
     return QTM_OK;
 }
@@ -641,11 +679,20 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     }
     const long long max_jumps = std::max<long long>(a->max_jumps, 0);
     const Variant& var = variants()[p->variant];
+    const bool bdf = p->method == 1;
+    const void* const kfn = bdf ? p->bdf_fn : var.fn;
+    const int kthreads = bdf ? p->bdf_threads : var.threads;
     int dev_sms = 0, per_sm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kthreads, p->smem));
     if (per_sm < 1) return set_error(QTM_ERR_CUDA, "kernel variant cannot be resident (registers/smem)");
-    const long long grid = std::min<long long>((long long)dev_sms * per_sm, std::min<long long>(count, 1ll << 16));
+    long long grid = std::min<long long>((long long)dev_sms * per_sm, std::min<long long>(count, 1ll << 16));
+    if (bdf && !p->bdf_in_smem) {
+        // HBM workspaces (d^2 LU per CTA): at most ~8 GB of them, >= 1 per SM
+        const long long cap = std::max<long long>(dev_sms, (8ll << 30) / (16ll * p->bdf_ws_elems));
+        grid = std::min(grid, cap);
+    }
+    if (bdf) o->variant = -1;
     o->grid = (int32_t)grid;
 
     // Large ensembles run in chunks of at most kRunChunk trajectories so the
@@ -656,7 +703,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     constexpr long long kRunChunk = 1ll << 16;
     constexpr int kRedChunk = 256;
     const long long run_chunk = std::min<long long>(count, kRunChunk);
-    const int nw = var.threads / 32;
+    const int nw = kthreads / 32;
     const int DP = var.threads * var.comps;
     const long long n_red_total = (count + kRedChunk - 1) / kRedChunk;
     CUDA_TRY(p->values.ensure((size_t)run_chunk * std::max(n_out, 1), s));
@@ -669,7 +716,8 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     CUDA_TRY(p->jump_t.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
     CUDA_TRY(p->jump_idx.ensure((size_t)run_chunk * std::max<long long>(max_jumps, 1), s));
     CUDA_TRY(p->stats_tot.ensure(QTM_NSTATS + 1, s));
-    if (var.reg_rows > 0 && var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
+    if (!bdf && var.reg_rows > 0 && var.reg_rows < LROWS) CUDA_TRY(p->zovf.ensure((size_t)grid * (LROWS - var.reg_rows) * DP, s));
+    if (bdf && !p->bdf_in_smem) CUDA_TRY(p->bdf_ws.ensure((size_t)grid * p->bdf_ws_elems, s));
     CUDA_TRY(p->psum.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->psq.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));
@@ -718,9 +766,13 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         R.counter = p->ctl.p;
         R.first_fail = p->ctl.p + 1;
         R.phase_cycles = p->ctl.p + 2;
-        void* kargs[] = {(void*)&p->dp, (void*)&R};
+        BdfParams BP{};
+        BP.ws = p->bdf_ws.p;
+        BP.ws_stride = p->bdf_ws_elems;
+        BP.in_smem = p->bdf_in_smem ? 1 : 0;
+        void* kargs[] = {(void*)&p->dp, (void*)&R, (void*)&BP};
         CUDA_TRY(cudaEventRecord(p->ev[1], s));
-        CUDA_TRY(cudaLaunchKernel(var.fn, dim3((unsigned)cgrid), dim3(var.threads), kargs, p->smem, s));
+        CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)cgrid), dim3(kthreads), kargs, p->smem, s));
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(p->ev[2], s));
         const long long cells = cnt * p->n_pts;
