@@ -209,13 +209,26 @@ def _sum_over_ranks(dist, torch, local, x, world):
     return float(t.item())
 
 
-def run_reference_arm(args, rank, world):
+def build_problem(args):
+    """The config's problem; ``--method bdf`` swaps in the BDF family (same
+    tolerances) -- the reference's general engine, ode.py:334-423."""
+    import dataclasses
+
     from paper_1810_03047_b200 import configs
+    from paper_1810_03047_b200.problem import OdeConfig
+    p = configs.build(args.config)
+    if args.method != "adams":
+        p = dataclasses.replace(p, ode=OdeConfig(method=args.method, rtol=p.ode.rtol,
+                                                 atol=p.ode.atol))
+    return p
+
+
+def run_reference_arm(args, rank, world):
     from paper_1810_03047_b200.packing import pack_problem
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    packed = pack_problem(configs.build(args.config))
+    packed = pack_problem(build_problem(args))
     sample = CPU_SAMPLE_PER_THREAD[args.config] * threads
     value, sec = cpu_reference(packed, sample, args.steps, args.warmup, threads)
     desc = (f"{sample} trajectories of {args.config} per step (global indices 0..{sample - 1}, "
@@ -225,7 +238,7 @@ def run_reference_arm(args, rank, world):
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "config": args.config,
-                       "trajectories_per_step": sample},
+                       "method": args.method, "trajectories_per_step": sample},
             "cpu_baseline": {"value": value, "unit": "trajectories/s", "cores": threads,
                              "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": "trajectories/s", "h2d_bytes_per_step": 0,
@@ -244,6 +257,8 @@ def main(argv=None):
     ap.add_argument("--variant", type=int, default=-2,
                     help="kernel variant (-1: by dimension, -2: autotune during warm-up)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--method", default="adams", choices=["adams", "bdf"],
+                    help="ODE method family (bdf: modified Newton with a dense LU per trajectory)")
     ap.add_argument("--trajectories", type=int, default=0,
                     help="override the config's trajectory count (exploration only)")
     args = ap.parse_args(argv)
@@ -277,7 +292,7 @@ def main(argv=None):
             # then goes through gloo (never the case on an 8-GPU box)
             dist.init_process_group("gloo")
     stream = torch.cuda.current_stream(local)
-    problem = configs.build(args.config)
+    problem = build_problem(args)
     packed = pack_problem(problem)
     n_total = (args.trajectories or N_TRAJECTORIES[args.config]) * \
         (world if args.scaling == "weak" else 1)
@@ -300,6 +315,8 @@ def main(argv=None):
     # start-up is over before the timed region
     clocks = ClockSampler(local)
     clocks.start()
+    if args.method == "bdf":
+        args.variant = -1  # one BDF kernel per block size (qtm_bdf.cuh)
     if args.variant == -2:  # untimed: choose the kernel variant on a sample
         args.variant = autotune_variant(packed, device=local)
     dp = DeviceProblem(packed, device=local, variant=args.variant)
@@ -390,12 +407,13 @@ def main(argv=None):
             "config": {"workload": WORKLOADS[args.config], "config": args.config,
                        "trajectories": n_total, "trajectories_per_gpu": end - begin,
                        "seed": SEED, "stream": "philox", "rtol": packed.rtol,
-                       "atol": packed.atol, "method": "adams",
+                       "atol": packed.atol, "method": args.method,
                        "l2": "256 MiB buffer overwritten between timed steps",
                        "failed_trajectories": n_failed,
                        "failure_note": "reference-faithful OdeFailure(-5) step collapses, "
                                        "excluded from value and averages",
-                       "kernel_variant": native.variants()[outs[-1].variant],
+                       "kernel_variant": (native.variants()[outs[-1].variant]
+                                          if outs[-1].variant >= 0 else "bdf_kernel"),
                        "grid_ctas": outs[-1].grid,
                        "history_rows": {"registers": layout["reg_rows"],
                                         "shared": layout["smem_rows"]},
@@ -407,7 +425,9 @@ def main(argv=None):
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": (profiled_traffic(args.config) or {}).get("bytes"),
                          "traffic_source": (profiled_traffic(args.config) or {}).get("source"),
-                         "kernel": "traj_kernel (persistent; state in registers/smem)",
+                         "kernel": ("traj_kernel (persistent; state in registers/smem)"
+                                    if args.method == "adams" else
+                                    "bdf_kernel (persistent; LU + Newton in smem/HBM workspace)"),
                          "peak_source": "measured DFMA throughput on this GPU "
                                         "(qtm_measure_fp64_peak, 2 flops/DFMA)",
                          "flops_per_launch": flops, "kernel_ms": k_ms,
@@ -416,7 +436,8 @@ def main(argv=None):
                                            "time; the kernel keeps state on chip"},
             "step_ms": [round(x, 3) for x in per_step],
             "work": {k: st[k] for k in ("attempts", "steps", "corr_iters", "jumps",
-                                        "corr_fail", "err_reject", "overflow_attempts")},
+                                        "corr_fail", "err_reject", "overflow_attempts",
+                                        "lu_factor")},
             "clocks": clk,
             "cpu_baseline": cpu,
         }

@@ -62,7 +62,7 @@ enum qtm_stat {
     QTM_STAT_ATTEMPTS = 0, QTM_STAT_STEPS, QTM_STAT_CORR_FAIL, QTM_STAT_ERR_REJECT,
     QTM_STAT_NFE, QTM_STAT_CORR_ITERS, QTM_STAT_JUMPS, QTM_STAT_BISECT, QTM_STAT_SUM_Q,
     QTM_STAT_ORDER_UP, QTM_STAT_ORDER_DOWN, QTM_STAT_DRAWS, QTM_STAT_SUM_QQ1,
-    QTM_STAT_OVERFLOW_ATTEMPTS
+    QTM_STAT_OVERFLOW_ATTEMPTS, QTM_STAT_LU_FACTOR  /* BDF: factorisations of I - h l0 G */
 };
 
 /* Square complex CSR operator in the reference layout (linalg.py:43-60):
@@ -87,12 +87,12 @@ typedef struct {
     double t_from, t_to;
     int64_t n_steps;           /* grid has n_steps + 1 points */
     const double* times;       /* [n_steps+1]  np.linspace(t_from, t_to, n_steps+1) */
-    int32_t method;            /* 0 = ADAMS (only value supported) */
+    int32_t method;            /* 0 = ADAMS (numba kernel path), 1 = BDF (modified Newton, ode.py:334-423) */
     double rtol, atol;
-    int32_t max_order;         /* 1..12 */
+    int32_t max_order;         /* 1..12 (ADAMS), 1..6 (BDF) */
     int64_t max_steps;
     double h0_first;           /* first-segment step: initial_step or auto step (ode.py:199-203) */
-    const double* l_table;     /* [13*13] Adams l-vectors, row q (ode.py:90-121) */
+    const double* l_table;     /* [13*13] l-vectors of the method, row q (ode.py:90-121) */
     const double* tau1;        /* [13] */
     const double* tau2;        /* [13] */
     const double* tau3;        /* [13] */

@@ -452,6 +452,7 @@ static double step_bdf(solver_t* S, int* status) {
         if (!(S->has_lu && !S->jac_stale && fabs(hl0 / S->hl0_fact - 1.0) <= 0.3)) {
             S->jac_stale = 0;
             bdf_factor(S, hl0);
+            S->st[MO_STAT_LU_FACTOR]++;
             S->has_lu = 1;
             S->hl0_fact = hl0;
             S->crate = 0.7;

@@ -31,7 +31,7 @@ enum {
 enum {
     MO_STAT_ATTEMPTS = 0, MO_STAT_STEPS, MO_STAT_CORR_FAIL, MO_STAT_ERR_REJECT, MO_STAT_NFE,
     MO_STAT_CORR_ITERS, MO_STAT_JUMPS, MO_STAT_BISECT, MO_STAT_SUM_Q, MO_STAT_ORDER_UP,
-    MO_STAT_ORDER_DOWN, MO_STAT_DRAWS, MO_NSTATS = 16
+    MO_STAT_ORDER_DOWN, MO_STAT_DRAWS, MO_STAT_LU_FACTOR = 14, MO_NSTATS = 16
 };
 
 typedef struct {

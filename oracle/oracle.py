@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libmcwf_oracle.so")
 
 NSTATS = 16
 STAT_NAMES = ("attempts", "steps", "corr_fail", "err_reject", "nfe", "corr_iters", "jumps",
-              "bisect", "sum_q", "order_up", "order_down", "draws")
+              "bisect", "sum_q", "order_up", "order_down", "draws", "", "", "lu_factor")
 STREAM_KINDS = {"philox": 0, "lfsr113": 1, "scripted": 2}
 
 _I64P = C.POINTER(C.c_int64)

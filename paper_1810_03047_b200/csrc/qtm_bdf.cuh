@@ -44,7 +44,7 @@ struct BdfParams {
 
 // workspace layout in double2 units (d = state dimension)
 struct BdfLayout {
-    long long z, save, ypred, z1p, ycur, dy, x, e0, e1, psi, w2, ipiv, lu, total;
+    long long z, save, ypred, z1p, ycur, dy, x, e0, e1, psi, w2, ipiv, rowat, pos, dflag, dk, lu, total;
     __host__ __device__ static BdfLayout make(long long d) {
         BdfLayout L{};
         long long o = 0;
@@ -59,7 +59,11 @@ struct BdfLayout {
         L.e1 = o;    o += d;
         L.psi = o;   o += d;
         L.w2 = o;    o += (d + 1) / 2;   // doubles
-        L.ipiv = o;  o += (d + 3) / 4;   // ints
+        L.ipiv = o;  o += (d + 3) / 4;   // ints: pivot row of step k (zgetrf ipiv)
+        L.rowat = o; o += (d + 3) / 4;   // ints: original row at position k after the interchanges
+        L.pos = o;   o += (d + 3) / 4;   // ints: position of row i after the interchanges
+        L.dflag = o; o += (d + 3) / 4;   // ints: branch of the division by U(k, k)
+        L.dk = o;    o += d;             // (rat, scl) of the division by U(k, k)
         L.lu = o;    o += d * d;         // column-major: A(i, j) at lu[j*d + i]
         L.total = o;
         return L;
@@ -85,7 +89,8 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
 // M = I - hl0 G from the CSR generator, factored in place (zgetf2 order)
 template <int NT>
 __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
-                           double hl0, double* s_pv, int* s_pi) {
+                           int* __restrict__ rowat, int* __restrict__ pos, int* __restrict__ dflag,
+                           double2* __restrict__ dk, double hl0, double* s_pv, int* s_pi) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = P.d;
@@ -155,20 +160,48 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         }
         __syncthreads();
     }
-}
-
-// x = M^{-1} b (zgetrs): b is overwritten (interchanges + forward sweep)
-template <int NT>
-__device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __restrict__ ipiv,
-                          double2* __restrict__ b, double2* __restrict__ x) {
-    const int tid = threadIdx.x;
-    __syncthreads();
+    // Solve-side constants, computed once per factorisation: pos[i] = where
+    // b[i] lands after zlaswp's sequential interchanges (the caller writes the
+    // residual pre-permuted), and the divisor-only part of cdiv_np(x, U(k,k))
+    // -- rat and scl depend on U(k, k) alone, so the back substitution needs
+    // no division and stays bit-identical to cdiv_np.
     if (tid == 0) {
+        for (int k = 0; k < d; ++k) rowat[k] = k;
         for (int k = 0; k < d; ++k) {
             const int p = ipiv[k];
-            if (p != k) { const double2 t = b[k]; b[k] = b[p]; b[p] = t; }
+            if (p != k) { const int t = rowat[k]; rowat[k] = rowat[p]; rowat[p] = t; }
         }
     }
+    for (int k = tid; k < d; k += NT) {
+        const double2 b = A[(long long)k * d + k];
+        const double abr = fabs(b.x), abi = fabs(b.y);
+        if (abr >= abi) {
+            if (abr == 0.0 && abi == 0.0) {
+                dflag[k] = 2;
+                dk[k] = make_double2(0.0, 0.0);
+            } else {
+                const double rat = b.y / b.x;
+                dflag[k] = 0;
+                dk[k] = make_double2(rat, 1.0 / (b.x + b.y * rat));
+            }
+        } else {
+            const double rat = b.x / b.y;
+            dflag[k] = 1;
+            dk[k] = make_double2(rat, 1.0 / (b.y + b.x * rat));
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < d; k += NT) pos[rowat[k]] = k;
+    __syncthreads();
+}
+
+// x = M^{-1} b (zgetrs).  b arrives already interchanged (the caller writes
+// row i of the residual at pos[i]) and is overwritten by the forward sweep.
+template <int NT>
+__device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
+                          const double2* __restrict__ dk, double2* __restrict__ b,
+                          double2* __restrict__ x) {
+    const int tid = threadIdx.x;
     __syncthreads();
     for (int k = 0; k < d; ++k) {
         const double2 bk = b[k];
@@ -183,8 +216,16 @@ __device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __res
     for (int k = d - 1; k >= 0; --k) {
         double2 xk = b[k];
         if (xk.x != 0.0 || xk.y != 0.0) {
+            // xk = cdiv_np(b[k], U(k, k)) with the divisor part precomputed
+            const double2 rs = dk[k];
+            const int fl = dflag[k];
+            if (fl == 0)
+                xk = make_double2((xk.x + xk.y * rs.x) * rs.y, (xk.y - xk.x * rs.x) * rs.y);
+            else if (fl == 1)
+                xk = make_double2((xk.x * rs.x + xk.y) * rs.y, (xk.y * rs.x - xk.x) * rs.y);
+            else
+                xk = make_double2(xk.x / 0.0, xk.y / 0.0);
             const double2* const ck = A + (long long)k * d;
-            xk = cdiv_np(xk, ck[k]);
             for (int i = tid; i < k; i += NT) {
                 const double2 a = ck[i], bi = b[i];
                 b[i] = make_double2(bi.x - (xk.x * a.x - xk.y * a.y), bi.y - (xk.x * a.y + xk.y * a.x));
@@ -236,6 +277,10 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
     double2* const PS = ws + L.psi;
     double* const W2 = reinterpret_cast<double*>(ws + L.w2);
     int* const IPIV = reinterpret_cast<int*>(ws + L.ipiv);
+    int* const ROWAT = reinterpret_cast<int*>(ws + L.rowat);
+    int* const POS = reinterpret_cast<int*>(ws + L.pos);
+    int* const DFLAG = reinterpret_cast<int*>(ws + L.dflag);
+    double2* const DK = ws + L.dk;
     double2* const A = ws + L.lu;
     int rphase = 0;
 
@@ -331,6 +376,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                 if (t + h == t) { rc = kErrStepCollapse; err0 = t; err1 = h; goto traj_done; }
                 st[sAttempts]++;
                 st[sSumQ] += q;
+                st[sSumQQ1] += q * (q + 1);
                 const double* const lv = P.l[q];
                 const double l0 = lv[0], conit = P.conit[q];
                 // weights, save, predict (ode.py:336-342)
@@ -351,7 +397,8 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                     const double hl0 = h * l0;
                     if (!(has_lu && !jac_stale && fabs(hl0 / hl0_fact - 1.0) <= 0.3)) {
                         jac_stale = false;
-                        bdf_factor<NT>(P, A, IPIV, hl0, s_pv, s_pi);
+                        bdf_factor<NT>(P, A, IPIV, ROWAT, POS, DFLAG, DK, hl0, s_pv, s_pi);
+                        st[sLuFactor]++;
                         has_lu = true;
                         hl0_fact = hl0;
                         crate = 0.7;
@@ -363,10 +410,10 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                         // resid = ycur - l0 * (h G ycur - z1pred) - ypred (left to right)
                         for (int i = tid; i < d; i += NT) {
                             const double2 f = row_dot(P.g, i, YC);
-                            DY[i] = csub(csub(YC[i], cscale(l0, csub(cscale(h, f), Z1[i]))), YP[i]);
+                            DY[POS[i]] = csub(csub(YC[i], cscale(l0, csub(cscale(h, f), Z1[i]))), YP[i]);
                         }
                         st[sNfe]++;
-                        bdf_solve<NT>(d, A, IPIV, DY, X);
+                        bdf_solve<NT>(d, A, DFLAG, DK, DY, X);
                         double acc = 0.0;
                         for (int i = tid; i < d; i += NT) {
                             const double2 xi = X[i];

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -596,6 +597,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         // Newton vectors, LU of the iteration matrix) goes to shared memory when
         // it fits, else to a per-CTA slice of HBM
         p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
+        if (const char* ev = getenv("QTM_BDF_THREADS")) {  // A/B experiments
+            const int v = atoi(ev);
+            if (v == 32 || v == 128 || v == 256) p->bdf_threads = v;
+        }
         p->bdf_fn = p->bdf_threads == 32 ? (const void*)bdf_kernel<32>
                     : p->bdf_threads == 128 ? (const void*)bdf_kernel<128> : (const void*)bdf_kernel<256>;
         p->bdf_ws_elems = BdfLayout::make(d->dim).total;

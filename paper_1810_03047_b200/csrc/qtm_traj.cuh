@@ -46,7 +46,7 @@ enum Status : int {
 
 enum Stat : int {
     sAttempts = 0, sSteps, sCorrFail, sErrReject, sNfe, sCorrIters, sJumps, sBisect, sSumQ,
-    sOrderUp, sOrderDown, sDraws, sSumQQ1, sOverflow,
+    sOrderUp, sOrderDown, sDraws, sSumQQ1, sOverflow, sLuFactor,
 };
 
 // one compiled kernel configuration (see build.py VARIANTS)

@@ -89,10 +89,19 @@ def stats_dict(row) -> dict:
 
 def flops_model(stats_total: dict, packed: PackedProblem) -> float:
     """Algorithmic FP64 flops of all step attempts:
-    per attempt m (8 nnz + 15 d) + d (q(q+1) + 4(q+1) + 13)."""
+    per attempt m (8 nnz + 15 d) + d (q(q+1) + 4(q+1) + 13).
+
+    BDF (modified Newton, ode.py:379-423): per Newton iteration the SpMV
+    (8 nnz), the two triangular solves (8 d^2) and the residual / update /
+    WRMS (16 d); per attempt the predict, error test and commit; per LU
+    factorisation of I - h l0 G 8/3 d^3 (complex rank-1 updates) + 2 nnz."""
     d, nnz = packed.dim, packed.g.nnz
     m = stats_total["corr_iters"]
     att = stats_total["attempts"]
+    if getattr(packed, "method", 0) == 1:
+        return float(m * (8 * nnz + 8 * d * d + 16 * d)
+                     + d * (stats_total["sum_qq1"] + 4 * (stats_total["sum_q"] + att) + 8 * att)
+                     + stats_total.get("lu_factor", 0) * (8.0 / 3.0 * d ** 3 + 2 * nnz))
     return float(m * (8 * nnz + 15 * d)
                  + d * (stats_total["sum_qq1"] + 4 * (stats_total["sum_q"] + att) + 13 * att))
 

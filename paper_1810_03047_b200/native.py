@@ -21,7 +21,7 @@ MAX_OPS = 32
 STREAM_KINDS = {"philox": 0, "lfsr113": 1, "scripted": 2}
 STAT_NAMES = ("attempts", "steps", "corr_fail", "err_reject", "nfe", "corr_iters", "jumps",
               "bisect", "sum_q", "order_up", "order_down", "draws", "sum_qq1",
-              "overflow_attempts")
+              "overflow_attempts", "lu_factor")
 
 # status codes (enum qtm_status)
 OK = 0

@@ -62,7 +62,14 @@ def test_create_rejects_bad_descriptor():
     assert "ABI" in native.last_error()
     desc.abi_version = native.ABI_VERSION
     desc.dim = 2
-    desc.method = 1  # BDF is not on the device
+    desc.method = 2  # neither ADAMS (0) nor BDF (1)
+    assert L.qtm_problem_create(C.byref(desc), C.byref(h)) == native.ERR_ARGS
+    assert "method" in native.last_error()
+    desc.method = 1
+    desc.max_order = 7  # BDF order <= 6 (ode.py:46)
+    assert L.qtm_problem_create(C.byref(desc), C.byref(h)) == native.ERR_ARGS
+    desc.max_order = 6
+    desc.dim = 10000  # dense LU of I - h l0 G: dim <= 8192
     assert L.qtm_problem_create(C.byref(desc), C.byref(h)) == native.ERR_UNSUPPORTED
 
 
