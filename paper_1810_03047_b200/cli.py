@@ -19,8 +19,9 @@ Inline and ``--gpus K`` runs integrate global trajectories 0..N-1 with the
 per-trajectory streams of the device (``--stream philox|lfsr113``); K GPUs
 take contiguous index ranges (one host thread per device; the C ABI runs
 without the GIL) and their sums are combined in device order.
-``--local-workers`` (the reference's CPU process farm) and ``--method bdf``
-are not offered: there is no CPU path here.
+``--method bdf`` runs the BDF kernel (modified Newton with a per-trajectory
+LU, csrc/qtm_bdf.cuh).  ``--local-workers`` (the reference's CPU process
+farm) is not offered: there is no CPU path here.
 """
 
 from __future__ import annotations
@@ -73,9 +74,8 @@ def build_problem(config: RunConfig):
     construction as the reference CLI, cli.py:52-63); c1..c5 are the
     benchmark configs, whose own grids and tolerances apply unless
     overridden."""
-    if config.method != ADAMS:
-        raise ValueError(f"method {config.method!r} is not available on the device "
-                         f"(Adams only)")
+    if config.method not in (ADAMS, BDF):
+        raise ValueError(f"unknown method {config.method!r}")
     options = RunOptions(only_final_trj=config.only_final_trj, output_target=config.output,
                          verbose=config.verbose)
     if config.problem in PROBLEM_BUILDERS:
@@ -87,6 +87,9 @@ def build_problem(config: RunConfig):
     if config.problem in configs.CONFIGS:
         import dataclasses
         p = configs.build(config.problem)
+        if config.method != ADAMS:
+            p = dataclasses.replace(p, ode=OdeConfig(method=config.method, rtol=p.ode.rtol,
+                                                     atol=p.ode.atol))
         return dataclasses.replace(
             p, options=options, t_from=config.t_from,
             t_to=config.t_to if config.t_to is not None else p.t_to,

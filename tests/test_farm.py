@@ -276,11 +276,17 @@ def test_reference_master_drives_gpu_worker(oracle_lib, tmp_path):
 
 # ---------------------------------------------------------------- CLI
 def test_cli_usage_errors(capsys):
-    assert cli.main(["--problem", "unitary", "--method", "bdf"]) == cli.EXIT_USAGE
-    assert "Adams only" in capsys.readouterr().err
     assert cli.main(["--problem", "unitary", "--connect", "x:1"]) == cli.EXIT_USAGE
     assert cli.main(["--problem", "nope"]) == cli.EXIT_USAGE
     assert cli.main(["--problem", "unitary", "--listen", "127.0.0.1:1"]) == cli.EXIT_USAGE
+
+
+def test_cli_method_bdf_builds_bdf_problems():
+    for name in ("unitary", "c2"):
+        c = cli.parse_args(["--problem", name, "--method", "bdf"])
+        p = cli.build_problem(c)
+        assert p.ode.method == "bdf" and p.ode.max_order == 6
+        assert pack_problem(p).method == 1
 
 
 def test_cli_defaults_follow_reference():

@@ -14,8 +14,13 @@ from paper_1810_03047_b200.packing import pack_problem
 pytestmark = pytest.mark.gpu
 
 
-def test_gpu_workers_match_oracle(oracle_lib):
+@pytest.mark.parametrize("method", ["adams", "bdf"])
+def test_gpu_workers_match_oracle(method, oracle_lib):
+    import dataclasses
+    from paper_1810_03047_b200.problem import OdeConfig
     p = configs.build("c2", log_jumps=True)
+    if method == "bdf":
+        p = dataclasses.replace(p, ode=OdeConfig(method="bdf", rtol=p.ode.rtol, atol=p.ode.atol))
     pairs = [farm.QueueTransport.pair(timeout=300) for _ in range(2)]
     ths = [threading.Thread(target=farm.run_gpu_worker, args=(pairs[r][1], p, r))
            for r in range(2)]
@@ -51,6 +56,16 @@ def test_cli_inline_and_two_device_split(tmp_path):
         b = np.loadtxt(out2, delimiter=",", skiprows=1)
         np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
     assert a[0, 1] == 1.0  # <n> of |1> at t = 0
+
+
+def test_cli_method_bdf(tmp_path, oracle_lib):
+    out = tmp_path / "b.csv"
+    assert cli.main(["--problem", "photon", "--trajectories", "64", "--method", "bdf",
+                     "--output", str(out)]) == 0
+    a = np.loadtxt(out, delimiter=",", skiprows=1)
+    c = cli.parse_args(["--problem", "photon", "--method", "bdf"])
+    ref = oracle_lib.run(pack_problem(cli.build_problem(c)), 987654321, 0, 64)
+    np.testing.assert_allclose(a[:, 1], ref["values"].mean(axis=0)[0], rtol=0, atol=1e-6)
 
 
 def test_cli_keep_trajectories(tmp_path):
