@@ -21,6 +21,11 @@
  *   - apply_collapse ................................... trajectory.py:133-154
  *   - record / record_expectation ...................... trajectory.py:122-130, 206-214
  *   - run_single_trajectory ............................ trajectory.py:190-250
+ *   Time-dependent right side (rhs_fn = a TimeDependentGenerator, run by the
+ *   reference's general engine with the Adams functional corrector,
+ *   ode.py:227-230, 334-377): every G y becomes G0 y + sum_k c_k(t) G_k y,
+ *   evaluated at t (cold start, restart) or t + h (corrector), in the
+ *   callable's order (timedep.py: G0 row sums, then + c_k * (G_k row) per k).
  *   BDF (method = MO_METHOD_BDF, the general engine with a CSR generator):
  *   - _attempt_general (save, predict, Newton, error test,
  *     commit / restore) ................................. ode.py:334-356
@@ -195,6 +200,26 @@ static void csr_matvec(const mo_csr* m, const cplx* x, cplx* out, int64_t n) {
     }
 }
 
+/* out = G(t) x: the constant generator, then the time-dependent terms */
+static double td_coef(const mo_problem* P, int k, double t) {
+    const double* c = P->td_coef + 4 * k;
+    return c[3] + c[0] * cos(c[1] * t + c[2]);
+}
+
+static void g_apply(const mo_problem* P, double t, const cplx* x, cplx* out, int64_t n) {
+    csr_matvec(&P->g, x, out, n);
+    for (int k = 0; k < P->n_td; ++k) {
+        const double c = td_coef(P, k, t);
+        const mo_csr* m = &P->td[k];
+        const cplx* v = (const cplx*)m->values;
+        for (int64_t i = 0; i < n; ++i) {
+            cplx s = {0.0, 0.0};
+            for (int64_t j = m->row_ptr[i]; j < m->row_ptr[i + 1]; ++j) s = cadd(s, cmul(v[j], x[m->col_ind[j]]));
+            out[i] = cadd(out[i], cscale(c, s));
+        }
+    }
+}
+
 /* (<psi|M|psi>, <psi|psi>) -- _kernels.py:30-41 */
 static void csr_quadform(const mo_csr* m, const cplx* psi, int64_t n, cplx* acc_out, double* nrm_out) {
     const cplx* v = (const cplx*)m->values;
@@ -321,6 +346,7 @@ static double step_kernel(solver_t* S, int* status) {
                 s = cadd(s, cmul(gv[j], ycur[P->g.col_ind[j]]));
             f[i] = s;
         }
+        if (P->n_td) g_apply(P, S->t + S->h, ycur, f, n);  /* G(t_new) ycur */
         S->st[MO_STAT_NFE]++;
         S->st[MO_STAT_CORR_ITERS]++;
         del = 0.0;
@@ -530,7 +556,7 @@ static void solver_restart_order_one(solver_t* S, double r) {
     S->q = 1;
     S->h *= r;
     S->has_lu = 0;
-    csr_matvec(&S->P->g, S->z, S->f, S->n);
+    g_apply(S->P, S->t, S->z, S->f, S->n);
     S->st[MO_STAT_NFE]++;
     for (int64_t i = 0; i < S->n; ++i) S->z[S->n + i] = cscale(S->h, S->f[i]);
     S->has_eprev = 0;
@@ -545,7 +571,7 @@ static void solver_cold_start(solver_t* S, double t0, const cplx* y0, double h0)
     S->q = 1;
     memset(S->z, 0, sizeof(cplx) * n * MO_LROWS);
     for (int64_t i = 0; i < n; ++i) S->z[i] = y0[i];
-    csr_matvec(&S->P->g, y0, S->f, n);
+    g_apply(S->P, t0, y0, S->f, n);
     S->st[MO_STAT_NFE]++;
     S->h = h0;
     for (int64_t i = 0; i < n; ++i) S->z[n + i] = cscale(S->h, S->f[i]);
@@ -833,6 +859,7 @@ int mo_run(const mo_problem* P, const mo_run_args* A, mo_run_out* O) {
     if (P->n_collapse > MO_MAX_OPS || P->n_expect > MO_MAX_OPS) return MO_ERR_ARGS;
     if (P->method != MO_METHOD_ADAMS && P->method != MO_METHOD_BDF) return MO_ERR_ARGS;
     if (P->method == MO_METHOD_BDF && P->max_order > MO_BDF_MAX_ORDER) return MO_ERR_ARGS;
+    if (P->n_td < 0 || (P->n_td > 0 && (P->method != MO_METHOD_ADAMS || !P->td || !P->td_coef))) return MO_ERR_ARGS;
     shared_t sh;
     sh.P = P; sh.A = A; sh.O = O; sh.next = 0; sh.first_fail = -1;
     pthread_mutex_init(&sh.mu, NULL);

@@ -61,6 +61,11 @@ typedef struct {
     const double* tau2;
     const double* tau3;
     int32_t method;         /* 0 = ADAMS (numba kernel path), 1 = BDF (modified Newton, dense LU) */
+    /* time-dependent right side G(t) = G + sum_k c_k(t) G_k with
+     * c_k(t) = offset + amp cos(omega t + phase)  (paper_1810_03047_b200/timedep.py) */
+    int32_t n_td;
+    const mo_csr* td;
+    const double* td_coef;  /* [n_td][4]: amp, omega, phase, offset */
 } mo_problem;
 
 enum { MO_METHOD_ADAMS = 0, MO_METHOD_BDF = 1 };

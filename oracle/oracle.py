@@ -37,7 +37,8 @@ class MoProblem(C.Structure):
                 ("t_to", C.c_double), ("n_steps", C.c_int64), ("times", _F64P),
                 ("rtol", C.c_double), ("atol", C.c_double), ("max_order", C.c_int32),
                 ("max_steps", C.c_int64), ("h0_first", C.c_double), ("l_table", _F64P),
-                ("tau1", _F64P), ("tau2", _F64P), ("tau3", _F64P), ("method", C.c_int32)]
+                ("tau1", _F64P), ("tau2", _F64P), ("tau3", _F64P), ("method", C.c_int32),
+                ("n_td", C.c_int32), ("td", C.POINTER(MoCsr)), ("td_coef", _F64P)]
 
 
 class MoRunArgs(C.Structure):
@@ -105,12 +106,16 @@ def run(packed, seed: int, traj_begin: int, traj_end: int, *, stream: str = "phi
     keep = []
     coll = (MoCsr * max(1, packed.n_collapse))(*[_csr(c, keep) for c in packed.collapse])
     expt = (MoCsr * max(1, packed.n_expect))(*[_csr(e, keep) for e in packed.expect])
+    td = tuple(getattr(packed, "td", ()))
+    tds = (MoCsr * max(1, len(td)))(*[_csr(m, keep) for m in td])
+    td_coef = getattr(packed, "td_coef", None)
     prob = MoProblem(packed.dim, _csr(packed.g, keep), packed.n_collapse, coll,
                      packed.n_expect, expt, _p(packed.psi0), packed.t_from, packed.t_to,
                      packed.n_steps, _p(packed.times), packed.rtol, packed.atol,
                      packed.max_order, packed.max_steps, packed.h0_first,
                      _p(packed.l_table), _p(packed.tau1), _p(packed.tau2), _p(packed.tau3),
-                     getattr(packed, "method", 0))
+                     getattr(packed, "method", 0), len(td), tds,
+                     _p(td_coef) if td_coef is not None else None)
     n = traj_end - traj_begin
     script_arr = script_len = None
     stride = 0

@@ -60,6 +60,8 @@ class PackedProblem:
     log_jumps: bool
     digest: int
     method: int = 0        # 0 = ADAMS, 1 = BDF (qtm_problem_desc.method)
+    td: tuple = ()         # time-dependent terms G_k (PackedCsr), timedep.py
+    td_coef: np.ndarray | None = None  # float64 [n_td*4]: amp, omega, phase, offset
 
     @property
     def n_expect(self) -> int:
@@ -73,9 +75,13 @@ class PackedProblem:
     def n_pts(self) -> int:
         return self.n_steps + 1
 
+    @property
+    def n_td(self) -> int:
+        return len(self.td)
+
     def nbytes(self) -> int:
         total = self.psi0.nbytes + self.times.nbytes
-        for m in (self.g, *self.collapse, *self.expect):
+        for m in (self.g, *self.collapse, *self.expect, *self.td):
             total += m.row_ptr.nbytes + m.col_ind.nbytes + m.values.nbytes
         return total
 
@@ -92,33 +98,52 @@ def pack_problem(problem, *, h0_first: float | None = None) -> PackedProblem:
     with either method family: ADAMS (the numba kernel path,
     _kernels.py:117-192) or BDF (modified Newton with a dense LU of
     I - h l0 G, ode.py:334-423); the l/tau tables follow the method."""
-    if getattr(problem, "generator", None) is None:
-        raise ValueError("device engine needs a constant generator; the time-dependent "
-                         "rhs_fn path is not on the device (SURVEY.md §8f)")
+    from .timedep import TimeDependentGenerator
     ode = problem.ode
     if ode.method not in (ADAMS, BDF):
         raise ValueError(f"unknown ODE method {ode.method!r}")
-    g = PackedCsr.from_csr(problem.generator.g)
+    gen = getattr(problem, "generator", None)
+    rhs = getattr(problem, "rhs_fn", None)
+    td, td_coef = (), None
+    if gen is not None:
+        g0 = gen.g
+    elif isinstance(rhs, TimeDependentGenerator):
+        # H(t) = H0 + sum_k c_k(t) H_k on the device (timedep.py); the general
+        # engine integrates it with the Adams functional corrector
+        # (ode.py:227-230, 358-377) -- BDF would need finite-difference
+        # Jacobians of the callback (ode.py:425-437), not on the device
+        if ode.method != ADAMS:
+            raise ValueError("time-dependent generators run with the ADAMS method only")
+        g0 = rhs.g0
+        td = tuple(PackedCsr.from_csr(m) for m, _ in rhs.terms)
+        td_coef = np.ascontiguousarray(np.concatenate([c.as_array() for _, c in rhs.terms]))
+    else:
+        raise ValueError("device engine needs a constant generator or a TimeDependentGenerator "
+                         "rhs_fn (an arbitrary rhs_fn callback cannot run on the GPU)")
+    g = PackedCsr.from_csr(g0)
     psi0 = np.ascontiguousarray(np.asarray(problem.psi0, dtype=np.complex128))
     dim = psi0.shape[0]
     if g.n != dim:
         raise ValueError(f"generator dim {g.n} != state dim {dim}")
     collapse = tuple(PackedCsr.from_csr(c) for c in problem.collapse_csr)
     expect = tuple(PackedCsr.from_csr(e) for e in problem.expect_csr)
-    for m in (*collapse, *expect):
+    for m in (*collapse, *expect, *td):
         if m.n != dim:
             raise ValueError("collapse/expect operators must be CSR of the state dim")
     times = np.linspace(problem.t_from, problem.t_to, problem.n_steps + 1)
     if h0_first is None:
         h0_first = ode.initial_step if ode.initial_step is not None else \
-            auto_step(problem.generator.g, psi0, ode.rtol, ode.atol)
+            auto_step(g0, psi0, ode.rtol, ode.atol,
+                      f0=None if not td else np.asarray(rhs(problem.t_from, psi0), np.complex128))
     l_tab, tau1, tau2, tau3 = method_tables(ode.method)
     log_jumps = bool(getattr(getattr(problem, "options", None), "log_jumps", False))
     digest = _digest([dim, g.row_ptr, g.col_ind, g.values,
                       *[a for m in (*collapse, *expect) for a in (m.row_ptr, m.col_ind, m.values)],
                       len(collapse), len(expect), psi0, problem.t_from, problem.t_to,
                       problem.n_steps, ode.rtol, ode.atol, ode.max_order, ode.max_steps,
-                      float(h0_first)] + ([ode.method] if ode.method != ADAMS else []))
+                      float(h0_first)] + ([ode.method] if ode.method != ADAMS else [])
+                     + [a for m in td for a in (m.row_ptr, m.col_ind, m.values)]
+                     + ([td_coef] if td else []))
     return PackedProblem(dim=dim, g=g, collapse=collapse, expect=expect,
                          psi0=psi0.view(np.float64).copy(), t_from=float(problem.t_from),
                          t_to=float(problem.t_to), n_steps=int(problem.n_steps), times=times,
@@ -126,4 +151,4 @@ def pack_problem(problem, *, h0_first: float | None = None) -> PackedProblem:
                          max_order=int(ode.max_order), max_steps=int(ode.max_steps),
                          h0_first=float(h0_first), l_table=np.ascontiguousarray(l_tab.ravel()),
                          tau1=tau1, tau2=tau2, tau3=tau3, log_jumps=log_jumps, digest=digest,
-                         method=0 if ode.method == ADAMS else 1)
+                         method=0 if ode.method == ADAMS else 1, td=td, td_coef=td_coef)

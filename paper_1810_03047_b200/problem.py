@@ -272,11 +272,13 @@ def method_tables(method: str):
     raise ValueError(f"unknown method {method!r}")
 
 
-def auto_step(g: CsrMatrix, y0: np.ndarray, rtol: float, atol: float) -> float:
+def auto_step(g, y0: np.ndarray, rtol: float, atol: float, f0=None) -> float:
     """Automatic first step h = 0.01 / ||G y0||_wrms with weights
     1/(atol + rtol |y0_i|) (ode.py:247-252), evaluated with the same numpy
-    expression (a BLAS dot) as the reference so the value matches it."""
-    f0 = csr_matvec(g, y0)
+    expression (a BLAS dot) as the reference so the value matches it.
+    ``f0`` overrides G y0 (a time-dependent right side at t_from)."""
+    if f0 is None:
+        f0 = csr_matvec(g, y0)
     w2 = 1.0 / (atol + rtol * np.abs(y0)) ** 2
     fw = sqrt(float((f0.real * f0.real + f0.imag * f0.imag) @ w2) / y0.shape[0])
     if fw <= 0.0:

@@ -61,14 +61,25 @@ def problem_arrays(p: QuantumProblem) -> dict:
            "n_collapse": len(p.collapse_csr), "n_expect": len(p.expect_csr)}
     if p.ode.method != "adams":
         out["method"] = p.ode.method
-    g = p.generator.g
+    if p.generator is None:  # TimeDependentGenerator rhs_fn (paper_1810_03047_b200/timedep.py)
+        gen = p.rhs_fn
+        g = gen.g0
+        out["n_td"] = len(gen.terms)
+        out["td_coef"] = np.concatenate([c.as_array() for _, c in gen.terms])
+        for k, (m, _) in enumerate(gen.terms):
+            out[f"td{k}_row_ptr"] = m.row_ptr
+            out[f"td{k}_col_ind"] = m.col_ind
+            out[f"td{k}_values"] = m.values
+    else:
+        g = p.generator.g
     out.update(g_row_ptr=g.row_ptr, g_col_ind=g.col_ind, g_values=g.values)
     for tag, ops in (("c", p.collapse_csr), ("e", p.expect_csr)):
         for i, m in enumerate(ops):
             out[f"{tag}{i}_row_ptr"] = m.row_ptr
             out[f"{tag}{i}_col_ind"] = m.col_ind
             out[f"{tag}{i}_values"] = m.values
-    out["h0"] = OdeSolver(p.ode, g, t0=p.t_from, y0=p.psi0.copy()).h
+    out["h0"] = OdeSolver(p.ode, g if p.generator is not None else p.rhs_fn,
+                          t0=p.t_from, y0=p.psi0.copy()).h
     return out
 
 
@@ -256,8 +267,62 @@ def main_bdf():
     print(f"bdf fixtures done in {time.time() - t0:.1f}s")
 
 
+def main_td():
+    """Time-dependent fixtures (``td_*.npz``): the reference's general Adams
+    engine (ode.py:334-377) driving a ``TimeDependentGenerator`` rhs_fn --
+    H(t) = H0 + sum_k c_k(t) H_k -- through ``run_single_trajectory``."""
+    from math import sqrt
+
+    from paper_1810_03047_b200 import timedep as ours_td
+    from paper_1810_03047_b200 import qops as ours_ops
+    from mcwf.linalg import dagger, tensor
+    from mcwf.operators import destroy, eye
+
+    t0 = time.time()
+    ode = OdeConfig(rtol=1e-8, atol=1e-10)
+
+    def td_problem(h0, h_terms, collapse, expect, psi0, t_to, n_steps):
+        gen = ours_td.TimeDependentGenerator.from_operators(
+            ours_ops.OperatorSet(h0, tuple(collapse), ()), h_terms)
+        return QuantumProblem(generator=None, rhs_fn=gen,
+                              collapse_csr=tuple(to_csr(c) for c in collapse),
+                              expect_csr=tuple(to_csr(e) for e in expect), psi0=psi0,
+                              t_from=0.0, t_to=t_to, n_steps=n_steps, ode=ode,
+                              options=RunOptions(log_jumps=True))
+
+    sm = sigma_minus()
+    rabi = td_problem(0.5 * sigma_z(), [(sigma_x(), ours_td.Coefficient(0.5, 1.0))],
+                      [sqrt(0.1) * sm], [sigma_z(), dagger(sm) @ sm], fock(2, 0), 20.0, 200)
+    save("td_rabi", rabi, [run_sample(rabi, "philox", list(range(64)), list(range(0, 201, 10)), 2),
+                           run_sample(rabi, "lfsr113", list(range(16)), [], 2)])
+    print(f"  td_rabi: {time.time() - t0:.1f}s")
+    a = destroy(20)
+    ad = dagger(a)
+    cav = td_problem(0.5 * (ad @ a), [(a + ad, ours_td.Coefficient(1.0, 0.5)),
+                                      (ad @ a, ours_td.Coefficient(0.2, 2.0, 0.3, 0.05))],
+                     [sqrt(0.5) * a], [ad @ a, (a + ad) / 2], fock(20, 0), 30.0, 300)
+    save("td_cavity", cav, [run_sample(cav, "philox", list(range(12)), list(range(0, 301, 30)), 2)])
+    print(f"  td_cavity: {time.time() - t0:.1f}s")
+    n_sites = 6
+
+    def site(op, i):
+        f = [eye(2)] * n_sites
+        f[i] = op
+        return tensor(*f)
+    sz = [site(sigma_z(), i) for i in range(n_sites)]
+    sx = sum(site(sigma_x(), i) for i in range(n_sites))
+    h0 = sum(-1.0 * (sz[i] @ sz[i + 1]) for i in range(n_sites - 1)) - 0.7 * sx
+    ising = td_problem(h0, [(-1.0 * sx, ours_td.Coefficient(0.3, 2.0))],
+                       [sqrt(0.05) * site(sm, i) for i in range(n_sites)], sz,
+                       fock(2 ** n_sites, 0), 10.0, 100)
+    save("td_ising", ising, [run_sample(ising, "philox", list(range(6)), list(range(0, 101, 20)), 6)])
+    print(f"td fixtures done in {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    if "--bdf" in sys.argv:
+    if "--td" in sys.argv:
+        main_td()
+    elif "--bdf" in sys.argv:
         main_bdf()
     else:
         main()

@@ -50,9 +50,16 @@ def load(name: str) -> Golden:
     ode = OdeConfig(method=method, rtol=float(z["prob_rtol"]), atol=float(z["prob_atol"]),
                     max_order=int(z["prob_max_order"]), max_steps=int(z["prob_max_steps"]),
                     initial_step=None if np.isnan(init) else init)
+    g0 = CsrMatrix(n, z["prob_g_row_ptr"], z["prob_g_col_ind"], z["prob_g_values"])
+    gen, rhs = EffectiveGenerator(g0), None
+    if "prob_n_td" in z:  # time-dependent right side (timedep.py)
+        from paper_1810_03047_b200.timedep import Coefficient, TimeDependentGenerator
+        coef = z["prob_td_coef"].reshape(-1, 4)
+        rhs = TimeDependentGenerator(g0, [(_csr(z, f"prob_td{k}", n), Coefficient(*map(float, coef[k])))
+                                          for k in range(int(z["prob_n_td"]))])
+        gen = None
     p = QuantumProblem(
-        generator=EffectiveGenerator(CsrMatrix(n, z["prob_g_row_ptr"], z["prob_g_col_ind"],
-                                               z["prob_g_values"])),
+        generator=gen, rhs_fn=rhs,
         collapse_csr=tuple(_csr(z, f"prob_c{i}", n) for i in range(int(z["prob_n_collapse"]))),
         expect_csr=tuple(_csr(z, f"prob_e{i}", n) for i in range(int(z["prob_n_expect"]))),
         psi0=z["prob_psi0"], t_from=float(z["prob_t_from"]), t_to=float(z["prob_t_to"]),
@@ -72,6 +79,7 @@ CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
 SCENARIOS = ("decay_forced_jump", "decay_no_jump", "decay_streams", "rabi_closed",
              "rabi_collapse", "photon", "unitary", "trilinear")
 
+TD_NAMES = ("td_rabi", "td_cavity", "td_ising")
 BDF_NAMES = ("bdf_c1", "bdf_c2", "bdf_c3", "bdf_stiff", "bdf_decay_forced_jump")
 
 SCRIPTS = {"decay_forced_jump": [[0.5, 0.3, 0.9999999]],

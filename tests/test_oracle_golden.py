@@ -108,3 +108,31 @@ def test_bdf_tables_match_generating_polynomials():
     np.testing.assert_allclose(l[2, :3], [2 / 3, 1.0, 1 / 3], rtol=0, atol=0)
     assert t2[2] == 4.5 and t1[2] == 1.0
     assert np.all(l[7:] == 0.0)
+
+
+# ---- time-dependent H(t) = H0 + sum_k c_k(t) H_k (rhs_fn, ode.py:334-377) ----
+@pytest.mark.parametrize("name", goldens.TD_NAMES)
+def test_oracle_matches_reference_time_dependent(name, oracle_lib):
+    g = goldens.load(name)
+    assert g.problem.generator is None and g.problem.rhs_fn is not None
+    assert pack_problem(g.problem).h0_first == g.h0  # auto step from G(t_from) psi0
+    for kind in g.samples:
+        _check(name, kind, oracle_lib)
+
+
+def test_time_dependent_generator_call_order():
+    """The rhs_fn callable adds c_k(t) (G_k psi) to G0 psi term by term --
+    the order the oracle and the device kernel use."""
+    from paper_1810_03047_b200.csr import csr_matvec
+    g = goldens.load("td_cavity")
+    gen = g.problem.rhs_fn
+    psi = g.problem.psi0 * (1 + 0.5j)
+    t = 1.234
+    want = csr_matvec(gen.g0, psi)
+    for m, c in gen.terms:
+        want = want + (c.offset + c.amp * np.cos(c.omega * t + c.phase)) * csr_matvec(m, psi)
+    np.testing.assert_array_equal(gen(t, psi), want)
+    with pytest.raises(ValueError, match="ADAMS"):
+        import dataclasses
+        from paper_1810_03047_b200.problem import OdeConfig
+        pack_problem(dataclasses.replace(g.problem, ode=OdeConfig(method="bdf")))
