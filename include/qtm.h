@@ -36,10 +36,11 @@
 extern "C" {
 #endif
 
-#define QTM_ABI_VERSION 1
+#define QTM_ABI_VERSION 2   /* 2: BDF method, time-dependent terms */
 #define QTM_LROWS 13      /* Nordsieck rows: Adams order <= 12 (ode.py:46) */
 #define QTM_MAX_OPS 32    /* collapse / expectation operators per problem */
 #define QTM_NSTATS 16
+#define QTM_MAX_TD_TERMS 8 /* time-dependent generator terms */
 
 enum qtm_stream_kind { QTM_STREAM_PHILOX = 0, QTM_STREAM_LFSR113 = 1, QTM_STREAM_SCRIPTED = 2 };
 
@@ -98,6 +99,13 @@ typedef struct {
     const double* tau3;        /* [13] */
     int32_t device;            /* CUDA device ordinal */
     int32_t variant;           /* -1 = automatic kernel selection, else a qtm_variant index */
+    /* Time-dependent right side (replaces QuantumProblem.rhs_fn for
+     * H(t) = H0 + sum_k c_k(t) H_k, trajectory.py:61, 186; ADAMS only):
+     * psi' = (G + sum_k c_k(t) G_k) psi with `generator` = G0 and
+     * c_k(t) = offset + amp cos(omega t + phase).  n_td = 0: constant G. */
+    int32_t n_td;              /* 0..QTM_MAX_TD_TERMS */
+    const qtm_csr* td;         /* [n_td] G_k = -i H_k */
+    const double* td_coef;     /* [n_td][4] amp, omega, phase, offset */
 } qtm_problem_desc;
 
 typedef struct qtm_problem qtm_problem;
@@ -168,6 +176,9 @@ int qtm_num_variants(void);
 /* describe kernel variant i: threads per trajectory CTA, components per
  * thread, register-resident Nordsieck rows */
 int qtm_variant_info(int i, int32_t* threads, int32_t* comps, int32_t* reg_rows);
+/* 1 if variant i was compiled with the time-dependent generator terms
+ * (required when n_td > 0), 0 if not, < 0 on a bad index */
+int qtm_variant_time_dependent(int i);
 int qtm_device_count(void);
 /* measured FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA):
  * the denominator of the FP64 roofline fraction bench.py reports */

@@ -125,7 +125,7 @@ int set_error(int code, const std::string& msg) {
 // One translation unit per variant (gen/variant_*.cu, written by build.py)
 // so the instantiations compile in parallel; gen/variant_table.inc lists them.
 struct Variant {
-    int threads, comps, reg_rows, min_blocks, auto_upto;
+    int threads, comps, reg_rows, min_blocks, auto_upto, td;
     size_t smem;
     const void* fn;
 };
@@ -140,17 +140,19 @@ const std::vector<Variant>& variants() {
     static const std::vector<Variant> v = [] {
         std::vector<Variant> out;
         for (const qtm::VariantDesc& d : qtm_variant_table())
-            out.push_back(Variant{d.threads, d.comps, d.reg_rows, d.min_blocks, d.auto_upto, d.smem, d.fn});
+            out.push_back(Variant{d.threads, d.comps, d.reg_rows, d.min_blocks, d.auto_upto, d.td, d.smem, d.fn});
         return out;
     }();
     return v;
 }
 
 // automatic choice: the variant flagged for the smallest dimension bound >= d
-int auto_variant(int64_t d) {
+// among those built with (td) or without the time-dependent terms
+int auto_variant(int64_t d, bool td) {
     int best = -1;
     for (int i = 0; i < (int)variants().size(); ++i) {
         const Variant& v = variants()[i];
+        if ((v.td != 0) != td) continue;
         if (v.auto_upto >= d && (best < 0 || v.auto_upto < variants()[best].auto_upto)) best = i;
     }
     return best;
@@ -486,6 +488,11 @@ int qtm_variant_info(int i, int32_t* threads, int32_t* comps, int32_t* reg_rows)
     return QTM_OK;
 }
 
+int qtm_variant_time_dependent(int i) {
+    if (i < 0 || i >= (int)variants().size()) return set_error(QTM_ERR_ARGS, "variant index out of range");
+    return variants()[i].td;
+}
+
 int qtm_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -500,6 +507,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (d->method != 0 && d->method != 1) return set_error(QTM_ERR_ARGS, "method must be 0 (ADAMS) or 1 (BDF)");
     if (d->method == 1 && d->max_order > BDF_ROWS - 1) return set_error(QTM_ERR_ARGS, "max_order must be in [1, 6] for BDF");
     if (d->method == 1 && d->dim > 8192) return set_error(QTM_ERR_UNSUPPORTED, "BDF: dense LU of I - h l0 G limited to dim <= 8192");
+    if (d->n_td < 0 || d->n_td > QTM_MAX_TD_TERMS || (d->n_td > 0 && (!d->td || !d->td_coef)))
+        return set_error(QTM_ERR_ARGS, "n_td must be in [0, 8] with td and td_coef given");
+    if (d->n_td > 0 && d->method != 0)
+        return set_error(QTM_ERR_UNSUPPORTED, "time-dependent generators run with the ADAMS method only");
     if (d->n_collapse < 0 || d->n_collapse > QTM_MAX_OPS || d->n_expect < 0 || d->n_expect > QTM_MAX_OPS)
         return set_error(QTM_ERR_UNSUPPORTED, "at most 32 collapse and 32 expectation operators");
     if (d->max_order < 1 || d->max_order > 12) return set_error(QTM_ERR_ARGS, "max_order must be in [1, 12]");
@@ -507,10 +518,12 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (!(d->h0_first > 0.0)) return set_error(QTM_ERR_ARGS, "h0_first must be positive");
     if (!d->l_table || !d->tau1 || !d->tau2 || !d->tau3) return set_error(QTM_ERR_ARGS, "Adams tables missing");
     // (BDF runs its own kernel, qtm_bdf.cuh; the Adams variant slot is unused)
-    int variant = d->method == 1 ? 0 : (d->variant >= 0 ? d->variant : auto_variant(d->dim));
+    int variant = d->method == 1 ? 0 : (d->variant >= 0 ? d->variant : auto_variant(d->dim, d->n_td > 0));
     if (variant < 0 || variant >= (int)variants().size())
         return set_error(QTM_ERR_UNSUPPORTED, "no kernel variant for this dimension");
     const Variant& var = variants()[variant];
+    if (d->method == 0 && d->n_td > 0 && !var.td)
+        return set_error(QTM_ERR_ARGS, "kernel variant built without time-dependent terms");
     if (d->method == 0 && (int64_t)var.threads * var.comps < d->dim)
         return set_error(QTM_ERR_ARGS, "kernel variant too small for this dimension");
 
@@ -566,6 +579,11 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     rc = upload_csr(p, d->generator, d->dim, &P.g, "generator");
     for (int c = 0; rc == QTM_OK && c < d->n_collapse; ++c) rc = upload_csr(p, d->collapse[c], d->dim, &P.c[c], "collapse");
     for (int k = 0; rc == QTM_OK && k < d->n_expect; ++k) rc = upload_csr(p, d->expect[k], d->dim, &P.e[k], "expect");
+    P.n_td = d->n_td;
+    for (int k = 0; rc == QTM_OK && k < d->n_td; ++k) {
+        rc = upload_csr(p, d->td[k], d->dim, &P.td[k], "time-dependent term");
+        for (int j = 0; j < 4; ++j) P.td_c[k][j] = d->td_coef[4 * k + j];
+    }
     if (rc == QTM_OK) {
         double2* psi0 = nullptr;
         double* times = nullptr;

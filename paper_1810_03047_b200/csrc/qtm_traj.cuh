@@ -36,6 +36,7 @@ namespace qtm {
 
 constexpr int LROWS = 13;
 constexpr int MAXOPS = 32;
+constexpr int MAXTD = 8;    // time-dependent generator terms (QTM_MAX_TD_TERMS)
 constexpr int KRED = 4;  // values carried by one block reduction
 constexpr int NSTATS = 16;
 
@@ -51,7 +52,7 @@ enum Stat : int {
 
 // one compiled kernel configuration (see build.py VARIANTS)
 struct VariantDesc {
-    int threads, comps, reg_rows, min_blocks, auto_upto;
+    int threads, comps, reg_rows, min_blocks, auto_upto, td;
     size_t smem;
     const void* fn;
 };
@@ -116,6 +117,11 @@ struct DevProblem {
     // est_down > keep_down[q] (when q > 1) and est_up > keep_up[q] (when
     // raising is possible): ((1/1.1 - 1e-6) / bias)^k, k = q+1, q, q+2
     double keep_same[LROWS], keep_down[LROWS], keep_up[LROWS];
+    // time-dependent right side G(t) = G + sum_k c_k(t) G_k (timedep.py):
+    // c_k(t) = td_c[k][3] + td_c[k][0] cos(td_c[k][1] t + td_c[k][2])
+    int n_td;
+    DevCsr td[MAXTD];
+    double td_c[MAXTD][4];
 };
 
 struct RunParams {
@@ -172,6 +178,21 @@ static __device__ __noinline__ double2 row_dot(const DevCsr& m, int i, const dou
         si = si + (v.x * xv.y + v.y * xv.x);
     }
     return make_double2(sr, si);
+}
+
+// Time-dependent right side: f_i + sum_k c_k(t) (G_k x)_i, the terms added
+// one by one in order (TimeDependentGenerator.__call__, timedep.py), with
+// c_k(t) = offset + amp cos(omega t + phase).  Not inlined: a cold call on
+// problems with H(t) only; the constant-generator hot loop carries one
+// uniform branch.
+static __device__ __noinline__ double2 td_apply(const DevProblem& P, double t, int i,
+                                               const double2* __restrict__ x, double2 f) {
+    for (int k = 0; k < P.n_td; ++k) {
+        const double c = P.td_c[k][3] + P.td_c[k][0] * cos(P.td_c[k][1] * t + P.td_c[k][2]);
+        const double2 g = row_dot(P.td[k], i, x);
+        f = make_double2(f.x + c * g.x, f.y + c * g.y);
+    }
+    return f;
 }
 
 // f = G x for this thread's E rows from the staged sliced-ELL copy: the E
@@ -692,7 +713,10 @@ struct TrajKernel {
 #define PH_MARK(k) do { } while (0)
 #endif
 
-template <int NT, int E, int RREG, int MINB>
+// TD: variant compiled with the time-dependent generator terms (td_apply
+// calls cost registers even when not taken, so constant-generator variants
+// are built without them)
+template <int NT, int E, int RREG, int MINB, bool TD>
 __global__ void __launch_bounds__(NT, MINB)
 traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R) {
     constexpr int DP = NT * E;
@@ -764,6 +788,19 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         gwidth = P.sell_w[warp];
         __syncthreads();
     }
+// f[E] = G(t) x (x gathered in shared memory): constant part, then the
+// time-dependent terms at time tt (ode.py: rhs(t_new, y) in the corrector,
+// rhs(t, y) at cold start / restart)
+#define GSPMV_T(xs, f, tt)                                                   \
+    do {                                                                     \
+        GSPMV(xs, f);                                                        \
+        if constexpr (TD) {                                                  \
+            if (P.n_td) {                                                    \
+                _Pragma("unroll") for (int e = 0; e < E; ++e)                \
+                    if (ACT(e)) f[e] = td_apply(P, (tt), II(e), (xs), f[e]); \
+            }                                                                \
+        }                                                                    \
+    } while (0)
 // f[E] = G x (x gathered in shared memory)
 #define GSPMV(xs, f)                                                         \
     do {                                                                     \
@@ -917,7 +954,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         GATHER(y0, xs__);                                                    \
         STAT(sNfe, 1);                                                       \
         double2 f__[E];                                                      \
-        GSPMV(xs__, f__);                                                    \
+        GSPMV_T(xs__, f__, t);                                               \
         _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
             H::at(z, 0, e) = (y0)[e];                                        \
             H::at(z, 1, e) = cscale(h, f__[e]);                              \
@@ -974,7 +1011,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         ws.c_it++;
                         double v[3] = {0.0, 0.0, 0.0};
                         double2 fg[E];
-                        GSPMV(cur, fg);
+                        GSPMV_T(cur, fg, t + h);
                         PH_MARK(3);  // [3] SpMV
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
@@ -1042,7 +1079,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         GATHER(y0c, xs);
                         STAT(sNfe, 1);
                         double2 fr[E];
-                        GSPMV(xs, fr);
+                        GSPMV_T(xs, fr, t);
 #pragma unroll
                         for (int e = 0; e < E; ++e) H::at(z, 1, e) = cscale(h, fr[e]);
                         has_eprev = false;
@@ -1267,6 +1304,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #undef ACT
 #undef GATHER
 #undef GSPMV
+#undef GSPMV_T
 #undef HORNER
 #undef RESCALE
 #undef FAIL

@@ -159,11 +159,12 @@ class DeviceProblem:
 
         coll = (native.QtmCsr * max(1, pk.n_collapse))(*[csr(c) for c in pk.collapse])
         expt = (native.QtmCsr * max(1, pk.n_expect))(*[csr(e) for e in pk.expect])
+        tds = (native.QtmCsr * max(1, pk.n_td))(*[csr(m) for m in pk.td])
         desc = native.QtmProblemDesc(
             native.ABI_VERSION, pk.dim, csr(pk.g), pk.n_collapse, coll, pk.n_expect, expt,
             _p(pk.psi0), pk.t_from, pk.t_to, pk.n_steps, _p(pk.times), pk.method, pk.rtol, pk.atol,
             pk.max_order, pk.max_steps, pk.h0_first, _p(pk.l_table), _p(pk.tau1), _p(pk.tau2),
-            _p(pk.tau3), device, variant)
+            _p(pk.tau3), device, variant, pk.n_td, tds, _p(pk.td_coef))
         handle = C.c_void_p()
         rc = L.qtm_problem_create(C.byref(desc), C.byref(handle))
         if rc != 0:
@@ -265,11 +266,13 @@ class DeviceProblem:
 _TUNED: dict = {}
 
 
-def candidate_variants(dim: int) -> list[int]:
+def candidate_variants(dim: int, time_dependent: bool = False) -> list[int]:
     """Kernel variants able to hold a state of this dimension without
-    wasting more than half of their lanes (the smallest fit always counts)."""
+    wasting more than half of their lanes (the smallest fit always counts),
+    among those built with / without the time-dependent terms."""
     vs = native.variants()
-    fits = [i for i, (t, e, _) in enumerate(vs) if t * e >= dim]
+    fits = [i for i, (t, e, _) in enumerate(vs)
+            if t * e >= dim and native.variant_time_dependent(i) == time_dependent]
     if not fits:
         return []
     smallest = min(vs[i][0] * vs[i][1] for i in fits)
@@ -286,7 +289,7 @@ def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | No
     key = (packed.digest, device)
     if key in _TUNED:
         return _TUNED[key]
-    cands = candidate_variants(packed.dim)
+    cands = candidate_variants(packed.dim, packed.n_td > 0)
     if len(cands) <= 1:
         _TUNED[key] = cands[0] if cands else -1
         return _TUNED[key]

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QTM_LIB") or os.path.join(HERE, "libqtm.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 NSTATS = 16
 LROWS = 13
 MAX_OPS = 32
@@ -53,7 +53,8 @@ class QtmProblemDesc(C.Structure):
                 ("times", _F64P), ("method", C.c_int32), ("rtol", C.c_double),
                 ("atol", C.c_double), ("max_order", C.c_int32), ("max_steps", C.c_int64),
                 ("h0_first", C.c_double), ("l_table", _F64P), ("tau1", _F64P), ("tau2", _F64P),
-                ("tau3", _F64P), ("device", C.c_int32), ("variant", C.c_int32)]
+                ("tau3", _F64P), ("device", C.c_int32), ("variant", C.c_int32),
+                ("n_td", C.c_int32), ("td", C.POINTER(QtmCsr)), ("td_coef", _F64P)]
 
 
 class QtmRunArgs(C.Structure):
@@ -80,7 +81,8 @@ class QtmRunOut(C.Structure):
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",
            "qtm_max_resident", "qtm_problem_layout",
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
-           "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles")
+           "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles",
+           "qtm_variant_time_dependent")
 
 _lib = None
 
@@ -119,6 +121,8 @@ def lib():
     L.qtm_num_variants.restype = C.c_int
     L.qtm_variant_info.argtypes = [C.c_int, _I32P, _I32P, _I32P]
     L.qtm_variant_info.restype = C.c_int
+    L.qtm_variant_time_dependent.argtypes = [C.c_int]
+    L.qtm_variant_time_dependent.restype = C.c_int
     L.qtm_device_count.argtypes = []
     L.qtm_device_count.restype = C.c_int
     if hasattr(L, "qtm_phase_cycles"):
@@ -144,6 +148,10 @@ def variants():
         L.qtm_variant_info(i, C.byref(t), C.byref(e), C.byref(r))
         out.append((t.value, e.value, r.value))
     return out
+
+
+def variant_time_dependent(i: int) -> bool:
+    return lib().qtm_variant_time_dependent(i) == 1
 
 
 def fp64_peak_tflops(device: int = 0) -> float:
