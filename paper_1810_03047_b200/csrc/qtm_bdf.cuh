@@ -27,8 +27,13 @@
 // sequential in the pivot index, so they run as CTA-wide sweeps with one
 // barrier per pivot; the trailing update walks columns by warp and rows by
 // lane (column-major storage: coalesced, conflict-free).  There are no
-// reductions inside the LU or the solves, so with -fmad=false they are
-// bit-identical to the oracle's restatement.
+// reductions inside the LU or the substitution solves, so with -fmad=false
+// they are bit-identical to the oracle's restatement.  From d = 48 up the
+// Newton solve applies the explicit inverse instead (bdf_invert, LAPACK
+// zgetri order after the same pivoted LU): one parallel matrix-vector
+// product per iteration instead of 2d barrier-separated substitution
+// steps; the result differs from the substitution at the rounding level,
+// as LAPACK's blocked zgetrs does.
 #pragma once
 #include "qtm_traj.cuh"
 
@@ -40,6 +45,7 @@ struct BdfParams {
     double2* ws;             // per-CTA workspaces in HBM (when not in shared memory)
     long long ws_stride;     // double2 elements per CTA workspace
     int in_smem;             // 1: the workspace is the kernel's dynamic shared memory
+    int inverse;             // 1: Newton solves apply M^{-1} (zgetri after zgetrf), 0: substitution
 };
 
 // workspace layout in double2 units (d = state dimension)
@@ -192,6 +198,87 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
     }
     __syncthreads();
     for (int k = tid; k < d; k += NT) pos[rowat[k]] = k;
+    __syncthreads();
+}
+
+// M^{-1} in place from its LU (LAPACK zgetri, unblocked): inv(U) column by
+// column (ztrti2), then inv(M) L = inv(U) from the last column back
+// (zgemv per column), then the column interchanges in reverse pivot order.
+// Every entry is a sequential dot product owned by one thread (rows by
+// thread, column-major storage: conflict-free), two barriers per column.
+// The Newton solve then is one parallel matrix-vector product instead of
+// 2d barrier-separated substitution steps.  t: d-vector scratch.
+template <int NT>
+__device__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict__ ipiv,
+                           double2* __restrict__ t) {
+    const int tid = threadIdx.x;
+    for (int j = 0; j < d; ++j) {
+        double2* const cj = A + (long long)j * d;
+        for (int i = tid; i < j; i += NT) t[i] = cj[i];
+        const double2 ujj = cdiv_np(make_double2(1.0, 0.0), cj[j]);  // read before thread 0 overwrites it
+        __syncthreads();
+        const double2 ajj = make_double2(-ujj.x, -ujj.y);
+        for (int i = tid; i < j; i += NT) {
+            double sr = 0.0, si = 0.0;
+            for (int k = i; k < j; ++k) {
+                const double2 u = A[(long long)k * d + i], v = t[k];
+                sr = sr + (u.x * v.x - u.y * v.y);
+                si = si + (u.x * v.y + u.y * v.x);
+            }
+            cj[i] = make_double2(ajj.x * sr - ajj.y * si, ajj.x * si + ajj.y * sr);
+        }
+        if (tid == 0) cj[j] = ujj;
+        __syncthreads();
+    }
+    for (int j = d - 1; j >= 0; --j) {
+        double2* const cj = A + (long long)j * d;
+        for (int i = j + 1 + tid; i < d; i += NT) {
+            t[i] = cj[i];
+            cj[i] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        if (j < d - 1) {
+            for (int i = tid; i < d; i += NT) {
+                double2 s = cj[i];
+                for (int k = j + 1; k < d; ++k) {
+                    const double2 a = A[(long long)k * d + i], w = t[k];
+                    s = make_double2(s.x - (a.x * w.x - a.y * w.y), s.y - (a.x * w.y + a.y * w.x));
+                }
+                cj[i] = s;
+            }
+        }
+        __syncthreads();
+    }
+    for (int j = d - 2; j >= 0; --j) {
+        const int jp = ipiv[j];
+        if (jp != j) {
+            double2* const cj = A + (long long)j * d;
+            double2* const cp = A + (long long)jp * d;
+            for (int i = tid; i < d; i += NT) {
+                const double2 a = cj[i];
+                cj[i] = cp[i];
+                cp[i] = a;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// x = M^{-1} b with the explicit inverse: row i summed over j in order
+template <int NT>
+__device__ void bdf_apply_inverse(int d, const double2* __restrict__ A, const double2* __restrict__ b,
+                                  double2* __restrict__ x) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    for (int i = tid; i < d; i += NT) {
+        double sr = 0.0, si = 0.0;
+        for (int j = 0; j < d; ++j) {
+            const double2 a = A[(long long)j * d + i], v = b[j];
+            sr = sr + (a.x * v.x - a.y * v.y);
+            si = si + (a.x * v.y + a.y * v.x);
+        }
+        x[i] = make_double2(sr, si);
+    }
     __syncthreads();
 }
 
@@ -398,6 +485,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                     if (!(has_lu && !jac_stale && fabs(hl0 / hl0_fact - 1.0) <= 0.3)) {
                         jac_stale = false;
                         bdf_factor<NT>(P, A, IPIV, ROWAT, POS, DFLAG, DK, hl0, s_pv, s_pi);
+                        if (B.inverse) bdf_invert<NT>(d, A, IPIV, X);
                         st[sLuFactor]++;
                         has_lu = true;
                         hl0_fact = hl0;
@@ -410,10 +498,14 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                         // resid = ycur - l0 * (h G ycur - z1pred) - ypred (left to right)
                         for (int i = tid; i < d; i += NT) {
                             const double2 f = row_dot(P.g, i, YC);
-                            DY[POS[i]] = csub(csub(YC[i], cscale(l0, csub(cscale(h, f), Z1[i]))), YP[i]);
+                            DY[B.inverse ? i : POS[i]] =
+                                csub(csub(YC[i], cscale(l0, csub(cscale(h, f), Z1[i]))), YP[i]);
                         }
                         st[sNfe]++;
-                        bdf_solve<NT>(d, A, DFLAG, DK, DY, X);
+                        if (B.inverse)
+                            bdf_apply_inverse<NT>(d, A, DY, X);
+                        else
+                            bdf_solve<NT>(d, A, DFLAG, DK, DY, X);
                         double acc = 0.0;
                         for (int i = tid; i < d; i += NT) {
                             const double2 xi = X[i];

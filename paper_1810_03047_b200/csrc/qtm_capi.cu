@@ -219,6 +219,7 @@ struct qtm_problem {
     const void* bdf_fn = nullptr;
     int bdf_threads = 0;
     bool bdf_in_smem = false;
+    bool bdf_inverse = true;     // Newton solves by the explicit inverse (QTM_BDF_SOLVE=lu|inv overrides)
     long long bdf_ws_elems = 0;  // double2 per CTA workspace
     DevBuf<double2> bdf_ws;
     std::mutex mu;
@@ -615,6 +616,12 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         // Newton vectors, LU of the iteration matrix) goes to shared memory when
         // it fits, else to a per-CTA slice of HBM
         p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
+        // Newton solves: substitution with the LU (zgetrs) for small d, where
+        // the matrix is refactored every few attempts; the explicit inverse
+        // (zgetri) from d = 48 up, where 2d barrier-separated substitution
+        // steps per solve dominate (c3 BDF: 2.5x; c2 (d = 20): 0.7x)
+        p->bdf_inverse = d->dim >= 48;
+        if (const char* ev = getenv("QTM_BDF_SOLVE")) p->bdf_inverse = strcmp(ev, "lu") != 0;
         if (const char* ev = getenv("QTM_BDF_THREADS")) {  // A/B experiments
             const int v = atoi(ev);
             if (v == 32 || v == 128 || v == 256) p->bdf_threads = v;
@@ -793,6 +800,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         BP.ws = p->bdf_ws.p;
         BP.ws_stride = p->bdf_ws_elems;
         BP.in_smem = p->bdf_in_smem ? 1 : 0;
+        BP.inverse = p->bdf_inverse ? 1 : 0;
         void* kargs[] = {(void*)&p->dp, (void*)&R, (void*)&BP};
         CUDA_TRY(cudaEventRecord(p->ev[1], s));
         CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)cgrid), dim3(kthreads), kargs, p->smem, s));
