@@ -96,3 +96,20 @@ def test_bdf_forced_jump_at_ln2():
         out = dp.run(0, 0, 1, stream="scripted", script=goldens.SCRIPTS["bdf_decay_forced_jump"],
                      max_jumps=4)
     assert out.jump_count[0] == 1 and abs(out.jump_t[0, 0] - np.log(2.0)) < 1e-6
+
+
+@pytest.mark.parametrize("mode", ["lu", "inv"])
+@pytest.mark.parametrize("name,n", [("bdf_c2", 64), ("cav150", 6)])
+def test_bdf_solve_modes_agree(mode, name, n, monkeypatch, oracle_lib):
+    """Substitution (zgetrs order, bit-identical LU + solve to the oracle)
+    and explicit-inverse (zgetri) Newton solves, forced either way."""
+    monkeypatch.setenv("QTM_BDF_SOLVE", mode)
+    p = goldens.load(name).problem if name.startswith("bdf_") else \
+        _cavity(int(name[3:]), t_to=5.0, n_steps=50)
+    pk = pack_problem(p)
+    with DeviceProblem(pk) as dp:
+        out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert out.rc == 0, out.error
+    ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
+    _compare(out, ref["values"], ref["jump_count"],
+             [ref["jump_t"][i] for i in range(n)], [ref["jump_idx"][i] for i in range(n)])
