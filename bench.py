@@ -44,6 +44,8 @@ WORKLOADS = {
     "c4": "c4: dissipative transverse-field Ising L=10 (d=1024, CSR 11 nnz/row), "
           "4096 trajectories, 101 output times",
     "c5": "c5: two coupled lossy Kerr cavities (d=900, CSR), 100000 trajectories, 401 output times",
+    "c4td": "c4td: c4 with a modulated transverse field h(t) = 0.7 + 0.3 cos(2t) "
+            "(time-dependent H, d=1024), 4096 trajectories, 101 output times",
 }
 METRIC = "trajectories/sec (ensemble <O>(t))"
 
@@ -174,7 +176,7 @@ def cpu_reference(packed, sample: int, steps: int, warmup: int, threads: int):
     return done / (sum(times) / len(times)), sum(times) / len(times)
 
 
-CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1}
+CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1, "c4td": 8}
 
 
 def profiled_traffic(config: str):

@@ -23,7 +23,7 @@ from .problem import OdeConfig, QuantumProblem, RunOptions
 from .qops import (OperatorSet, coherent, destroy, eye, fock, sigma_minus, sigma_x,
                    sigma_z)
 
-__all__ = ["BASELINE_ODE", "CONFIGS", "N_TRAJECTORIES", "DENSE", "build"]
+__all__ = ["BASELINE_ODE", "CONFIGS", "EXTRA", "N_TRAJECTORIES", "DENSE", "build"]
 
 BASELINE_ODE = OdeConfig(rtol=1e-8, atol=1e-10)
 N_TRAJECTORIES = {"c1": 500, "c2": 5_000, "c3": 20_000, "c4": 4_096, "c5": 100_000}
@@ -93,10 +93,35 @@ def c5(log_jumps=False, ode=None):
     return _mk(ops, fock(900, 0), 40.0, 400, log_jumps, ode)
 
 
+def c4td(log_jumps=False, ode=None):
+    """c4 with a modulated transverse field (time-dependent H, timedep.py):
+    H(t) = -sum sz_i sz_{i+1} - h(t) sum sx_i, h(t) = 0.7 + 0.3 cos(2 t) --
+    the static part in G0, the modulation as one term c(t) = 0.3 cos(2 t)
+    on -sum sx_i.  Not a BASELINE config: the measured case of the H(t) row."""
+    from .timedep import Coefficient, TimeDependentGenerator
+    n_sites = 10
+    sz = [_site(sigma_z(), i) for i in range(n_sites)]
+    sx = sum(_site(sigma_x(), i) for i in range(n_sites))
+    h0 = sum(-1.0 * (sz[i] @ sz[i + 1]) for i in range(n_sites - 1)) - 0.7 * sx
+    collapse = tuple(sqrt(0.05) * _site(sigma_minus(), i) for i in range(n_sites))
+    gen = TimeDependentGenerator.from_operators(OperatorSet(h0, collapse, ()),
+                                                [(-1.0 * sx, Coefficient(0.3, 2.0))])
+    from .csr import to_csr
+    return QuantumProblem(generator=None, rhs_fn=gen,
+                          collapse_csr=tuple(to_csr(c) for c in collapse),
+                          expect_csr=tuple(to_csr(z) for z in sz), psi0=fock(1024, 0),
+                          t_from=0.0, t_to=10.0, n_steps=100, ode=ode or BASELINE_ODE,
+                          options=RunOptions(log_jumps=log_jumps))
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+EXTRA = {"c4td": c4td}
+N_TRAJECTORIES["c4td"] = 4_096
 
 
 def build(name: str, **kw) -> QuantumProblem:
+    if name in EXTRA:
+        return EXTRA[name](**kw)
     if name not in CONFIGS:
         raise ValueError(f"unknown config {name!r}; expected one of {sorted(CONFIGS)}")
     return CONFIGS[name](**kw)

@@ -92,6 +92,28 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// cj[i] -= ck[i] * ukj for rows i = lo + lane, lo + lane + 32, ... < d: four
+// rows in flight per lane (the loads of an HBM/L2-resident workspace would
+// otherwise serialise on their latency for large d); same per-element
+// arithmetic as the plain loop
+__device__ __forceinline__ void col_axpy(double2* __restrict__ cj, const double2* __restrict__ ck,
+                                         double2 ukj, int lo, int d, int lane) {
+    int i = lo + lane;
+    for (; i + 96 < d; i += 128) {
+        double2 l[4], a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { l[r] = ck[i + 32 * r]; a[r] = cj[i + 32 * r]; }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            cj[i + 32 * r] = make_double2(a[r].x - (l[r].x * ukj.x - l[r].y * ukj.y),
+                                          a[r].y - (l[r].x * ukj.y + l[r].y * ukj.x));
+    }
+    for (; i < d; i += 32) {
+        const double2 l = ck[i], a = cj[i];
+        cj[i] = make_double2(a.x - (l.x * ukj.x - l.y * ukj.y), a.y - (l.x * ukj.y + l.y * ukj.x));
+    }
+}
+
 // M = I - hl0 G from the CSR generator, factored in place (zgetf2 order)
 template <int NT>
 __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
@@ -157,12 +179,7 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         // trailing update: A(i, j) -= L(i, k) U(k, j), columns by warp, rows by lane
         for (int j = k + 1 + warp; j < d; j += NW) {
             double2* const cj = A + (long long)j * d;
-            const double2 ukj = cj[k];
-            for (int i = k + 1 + lane; i < d; i += 32) {
-                const double2 l = ck[i];
-                const double2 a = cj[i];
-                cj[i] = make_double2(a.x - (l.x * ukj.x - l.y * ukj.y), a.y - (l.x * ukj.y + l.y * ukj.x));
-            }
+            col_axpy(cj, ck, cj[k], k + 1, d, lane);
         }
         __syncthreads();
     }
@@ -220,6 +237,7 @@ __device__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict
         const double2 ajj = make_double2(-ujj.x, -ujj.y);
         for (int i = tid; i < j; i += NT) {
             double sr = 0.0, si = 0.0;
+#pragma unroll 4
             for (int k = i; k < j; ++k) {
                 const double2 u = A[(long long)k * d + i], v = t[k];
                 sr = sr + (u.x * v.x - u.y * v.y);
@@ -240,6 +258,7 @@ __device__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict
         if (j < d - 1) {
             for (int i = tid; i < d; i += NT) {
                 double2 s = cj[i];
+#pragma unroll 4
                 for (int k = j + 1; k < d; ++k) {
                     const double2 a = A[(long long)k * d + i], w = t[k];
                     s = make_double2(s.x - (a.x * w.x - a.y * w.y), s.y - (a.x * w.y + a.y * w.x));
@@ -272,6 +291,7 @@ __device__ void bdf_apply_inverse(int d, const double2* __restrict__ A, const do
     __syncthreads();
     for (int i = tid; i < d; i += NT) {
         double sr = 0.0, si = 0.0;
+#pragma unroll 4
         for (int j = 0; j < d; ++j) {
             const double2 a = A[(long long)j * d + i], v = b[j];
             sr = sr + (a.x * v.x - a.y * v.y);
