@@ -182,17 +182,15 @@ static __device__ __noinline__ double2 row_dot(const DevCsr& m, int i, const dou
 
 // Time-dependent right side: f_i + sum_k c_k(t) (G_k x)_i, the terms added
 // one by one in order (TimeDependentGenerator.__call__, timedep.py), with
-// c_k(t) = offset + amp cos(omega t + phase).  Not inlined: a cold call on
-// problems with H(t) only; the constant-generator hot loop carries one
-// uniform branch.
-static __device__ __noinline__ double2 td_apply(const DevProblem& P, double t, int i,
-                                               const double2* __restrict__ x, double2 f) {
-    for (int k = 0; k < P.n_td; ++k) {
-        const double c = P.td_c[k][3] + P.td_c[k][0] * cos(P.td_c[k][1] * t + P.td_c[k][2]);
-        const double2 g = row_dot(P.td[k], i, x);
-        f = make_double2(f.x + c * g.x, f.y + c * g.y);
-    }
-    return f;
+// c_k(t) = offset + amp cos(omega t + phase) evaluated once per product.
+// Only the TD kernel variants carry these calls.
+static __device__ __noinline__ double td_coef(const DevProblem& P, int k, double t) {
+    return P.td_c[k][3] + P.td_c[k][0] * cos(P.td_c[k][1] * t + P.td_c[k][2]);
+}
+__device__ __forceinline__ double2 td_term(const DevCsr& m, double c, int i, const double2* __restrict__ x,
+                                           double2 f) {
+    const double2 g = row_dot(m, i, x);
+    return make_double2(f.x + c * g.x, f.y + c * g.y);
 }
 
 // f = G x for this thread's E rows from the staged sliced-ELL copy: the E
@@ -795,9 +793,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     do {                                                                     \
         GSPMV(xs, f);                                                        \
         if constexpr (TD) {                                                  \
-            if (P.n_td) {                                                    \
+            for (int k__ = 0; k__ < P.n_td; ++k__) {                         \
+                const double c__ = td_coef(P, k__, (tt));                    \
                 _Pragma("unroll") for (int e = 0; e < E; ++e)                \
-                    if (ACT(e)) f[e] = td_apply(P, (tt), II(e), (xs), f[e]); \
+                    if (ACT(e)) f[e] = td_term(P.td[k__], c__, II(e), (xs), f[e]); \
             }                                                                \
         }                                                                    \
     } while (0)

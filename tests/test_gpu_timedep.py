@@ -62,3 +62,21 @@ def test_td_run_gpu_and_variant_guard(oracle_lib):
     plain = next(i for i in range(len(native.variants())) if not native.variant_time_dependent(i))
     with pytest.raises(RuntimeError, match="time-dependent"):
         DeviceProblem(g.problem, variant=plain)
+
+
+@pytest.mark.parametrize("variant", [-1, 36, 37])
+def test_td_c4td_variants_match_oracle(variant, oracle_lib):
+    """c4td (bench workload): the automatic TD variant and the shapes the
+    autotune can pick for d = 1024 / 900, vs the oracle."""
+    from paper_1810_03047_b200 import configs
+    assert native.variant_time_dependent(36) and native.variant_time_dependent(37)
+    pk = pack_problem(configs.build("c4td"))
+    n = 48
+    with DeviceProblem(pk, variant=variant) as dp:
+        out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
+    ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert out.rc == ref["rc"]
+    ok = ref["status"] == 0
+    np.testing.assert_array_equal(out.status, ref["status"])
+    np.testing.assert_array_equal(out.jump_count[ok], ref["jump_count"][ok])
+    np.testing.assert_allclose(out.values[ok], ref["values"][ok], rtol=0, atol=TOL)
