@@ -80,3 +80,14 @@ def test_td_c4td_variants_match_oracle(variant, oracle_lib):
     np.testing.assert_array_equal(out.status, ref["status"])
     np.testing.assert_array_equal(out.jump_count[ok], ref["jump_count"][ok])
     np.testing.assert_allclose(out.values[ok], ref["values"][ok], rtol=0, atol=TOL)
+
+
+@pytest.mark.parametrize("variant", [28, 30, 37])
+def test_td_other_variants_match_oracle(variant, oracle_lib):
+    pk = pack_problem(goldens.load("td_cavity").problem)
+    n = 64
+    with DeviceProblem(pk, variant=variant) as dp:
+        out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert out.rc == 0, out.error
+    ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
+    _compare(out, ref["values"], ref["jump_count"], list(ref["jump_t"]), list(ref["jump_idx"]))
