@@ -84,6 +84,13 @@ struct DevProblem {
     const double2* sell_dict;
     const int* sell_off;    // [DP/32] first entry of each slice
     const int* sell_w;      // [DP/32] width of each slice
+    // TD variants with one time-dependent term: the SELL above is built on
+    // the union pattern of G0 and G1, and sell_td_ent (uint16 per slot, same
+    // slot layout) holds the byte offset of G1's value in sell_td_dict
+    // (offset 0 = 0.0); both staged after the G0 entries
+    int sell_td, sell_td_dict_n;
+    const double2* sell_td_dict;
+    const uint16_t* sell_td_ent;
     // observables that are diagonal in the basis (number operators, sigma_z):
     // bit k of e_diag_mask set => dense values at e_diag[k * DP + i]
     unsigned e_diag_mask;
@@ -281,6 +288,42 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] = make_double2(sr[e], si[e]);
+}
+
+// G0 x and G1 x in one pass over the union-pattern SELL (TD variants with a
+// single time-dependent term): each row of each product is summed in column
+// order, as csr_matvec sums the row (zero-valued slots add exact zeros).
+template <int NT, int E>
+__device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, const double2* __restrict__ dict,
+                                             const uint16_t* __restrict__ tent, const double2* __restrict__ tdict,
+                                             const int (&off)[E], int width, const double2* __restrict__ x,
+                                             double2 (&out0)[E], double2 (&out1)[E]) {
+    const int lane = threadIdx.x & 31;
+    const char* const xb = reinterpret_cast<const char*>(x);
+    const char* const db = reinterpret_cast<const char*>(dict);
+    const char* const tb = reinterpret_cast<const char*>(tdict);
+    double sr[E], si[E], tr[E], ti[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; tr[e] = 0.0; ti[e] = 0.0; }
+    for (int k = 0; k < width; ++k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int slot = off[e] + k * 32 + lane;
+            const uint32_t u = ent[slot];
+            const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
+            const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
+            const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
+            sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
+            si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
+            tr[e] = tr[e] + (w.x * xv.x - w.y * xv.y);
+            ti[e] = ti[e] + (w.x * xv.y + w.y * xv.x);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        out0[e] = make_double2(sr[e], si[e]);
+        out1[e] = make_double2(tr[e], ti[e]);
+    }
 }
 
 // One lane-halving level of a multi-value warp reduction: lanes with bit m
@@ -763,6 +806,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
                                                        TrajKernel<NT, E, RREG>::smem_bytes());
     uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_dict + P.sell_dict_n);
+    double2* const s_tdict = reinterpret_cast<double2*>(s_ent + P.sell_entries);
+    uint16_t* const s_tent = reinterpret_cast<uint16_t*>(s_tdict + P.sell_td_dict_n);
     // ---- stage the diagonal observables' index + dictionary tables
     const uint8_t* const s_eidx = reinterpret_cast<const uint8_t*>(smem) + P.e_stage_off;
     const double* const s_edict = reinterpret_cast<const double*>(s_eidx + P.e_stage_idx_bytes);
@@ -780,6 +825,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
+        if (TD && P.sell_td) {
+            for (int i = tid; i < P.sell_td_dict_n; i += NT) s_tdict[i] = P.sell_td_dict[i];
+            for (int i = tid; i < P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
+        }
         const int warp = tid >> 5;
 #pragma unroll
         for (int e = 0; e < E; ++e) goff[e] = P.sell_off[warp + (NT / 32) * e];
@@ -791,6 +840,16 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 // rhs(t, y) at cold start / restart)
 #define GSPMV_T(xs, f, tt)                                                   \
     do {                                                                     \
+        if constexpr (TD) {                                                  \
+            if (P.sell_td) {                                                 \
+                double2 g__[E];                                              \
+                sell_spmv_td<NT, E>(s_ent, s_dict, s_tent, s_tdict, goff, gwidth, (xs), f, g__); \
+                const double c__ = td_coef(P, 0, (tt));                      \
+                _Pragma("unroll") for (int e = 0; e < E; ++e)                \
+                    f[e] = make_double2(f[e].x + c__ * g__[e].x, f[e].y + c__ * g__[e].y); \
+                break;                                                       \
+            }                                                                \
+        }                                                                    \
         GSPMV(xs, f);                                                        \
         if constexpr (TD) {                                                  \
             for (int k__ = 0; k__ < P.n_td; ++k__) {                         \
