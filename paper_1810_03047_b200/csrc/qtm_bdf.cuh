@@ -115,10 +115,158 @@ __device__ __forceinline__ void col_axpy(double2* __restrict__ cj, const double2
 }
 
 // M = I - hl0 G from the CSR generator, factored in place (zgetf2 order)
+// izamax over rows k..d-1 of column ck: the first row of maximal |re| + |im|
+// (every thread gets the same answer)
+template <int NT>
+__device__ __forceinline__ int pivot_row(const double2* __restrict__ ck, int k, int d, double* s_pv, int* s_pi) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double bv = -1.0;
+    int bi = d;
+    for (int i = k + tid; i < d; i += NT) {
+        const double2 a = ck[i];
+        const double v = fabs(a.x) + fabs(a.y);
+        if (v > bv) { bv = v; bi = i; }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, m);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if constexpr (NW > 1) {
+        if (lane == 0) { s_pv[warp] = bv; s_pi[warp] = bi; }
+        __syncthreads();
+        bv = s_pv[0];
+        bi = s_pi[0];
+        for (int w = 1; w < NW; ++w)
+            if (s_pv[w] > bv || (s_pv[w] == bv && s_pi[w] < bi)) { bv = s_pv[w]; bi = s_pi[w]; }
+    }
+    return bi < d ? bi : k;
+}
+
+constexpr int LU_NB = 32;        // panel width of the blocked LU
+constexpr int LU_MB = 64;        // rows of a trailing-update tile
+// shared memory of the blocked LU's trailing-update tiles (double2 units)
+constexpr int LU_TILE_ELEMS = LU_NB * LU_MB + LU_NB * 32;
+
+// Blocked right-looking LU (LAPACK zgetrf structure) for a matrix that lives
+// in HBM: per panel of LU_NB columns the unblocked factorisation restricted
+// to the panel, the panel's row interchanges on the other columns, the
+// triangular solve for the panel rows of the trailing columns, and the
+// trailing update in LU_MB x 32 tiles staged through shared memory (each
+// entry read and written once per panel instead of once per pivot).  Every
+// entry still receives its updates one product at a time in pivot order,
+// and the interchanges commute with the row-wise updates, so the result is
+// bit-identical to the unblocked sweep.  Requires NT = 256.
+template <int NT>
+__device__ void lu_blocked(double2* __restrict__ A, int* __restrict__ ipiv, int d, double2* tiles,
+                           double* s_pv, int* s_pi) {
+    static_assert(NT == 256, "tile mapping assumes 8 warps");
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double2* const sL = tiles;                   // [LU_NB][LU_MB]
+    double2* const sU = tiles + LU_NB * LU_MB;   // [LU_NB][32]
+    for (int k0 = 0; k0 < d; k0 += LU_NB) {
+        const int kend = min(k0 + LU_NB, d), kb = kend - k0;
+        // ---- panel: unblocked steps on columns k0..kend-1
+        for (int k = k0; k < kend; ++k) {
+            double2* const ck = A + (long long)k * d;
+            const int p = pivot_row<NT>(ck, k, d, s_pv, s_pi);
+            if (tid == 0) ipiv[k] = p;
+            const double2 piv = ck[p];
+            __syncthreads();
+            if (piv.x != 0.0 || piv.y != 0.0) {
+                if (p != k && tid < kb) {
+                    double2* const cj = A + (long long)(k0 + tid) * d;
+                    const double2 t = cj[k];
+                    cj[k] = cj[p];
+                    cj[p] = t;
+                }
+                const double2 rcp = cdiv_np(make_double2(1.0, 0.0), piv);
+                __syncthreads();
+                for (int i = k + 1 + tid; i < d; i += NT) ck[i] = cmul2(ck[i], rcp);
+            }
+            __syncthreads();
+            for (int j = k + 1 + warp; j < kend; j += NW) {
+                double2* const cj = A + (long long)j * d;
+                col_axpy(cj, ck, cj[k], k + 1, d, lane);
+            }
+            __syncthreads();
+        }
+        // ---- the panel's interchanges on every other column (zlaswp)
+        for (int j = tid; j < d; j += NT) {
+            if (j >= k0 && j < kend) continue;
+            double2* const cj = A + (long long)j * d;
+            for (int k = k0; k < kend; ++k) {
+                const int p = ipiv[k];
+                if (p != k) { const double2 t = cj[k]; cj[k] = cj[p]; cj[p] = t; }
+            }
+        }
+        __syncthreads();
+        if (kend >= d) break;
+        // ---- U12: panel rows of the trailing columns (unit-lower solve, ztrsm)
+        for (int j = kend + tid; j < d; j += NT) {
+            double2* const cj = A + (long long)j * d;
+            for (int k = k0 + 1; k < kend; ++k) {
+                double2 s = cj[k];
+                for (int kp = k0; kp < k; ++kp) {
+                    const double2 l = A[(long long)kp * d + k], u = cj[kp];
+                    s = make_double2(s.x - (l.x * u.x - l.y * u.y), s.y - (l.x * u.y + l.y * u.x));
+                }
+                cj[k] = s;
+            }
+        }
+        __syncthreads();
+        // ---- A22 -= L21 U12, tile by tile, products subtracted in pivot order
+        for (int rb = kend; rb < d; rb += LU_MB) {
+            for (int idx = tid; idx < kb * LU_MB; idx += NT) {
+                const int k = idx / LU_MB, r = idx - k * LU_MB;
+                sL[k * LU_MB + r] = rb + r < d ? A[(long long)(k0 + k) * d + rb + r] : make_double2(0.0, 0.0);
+            }
+            for (int cb = kend; cb < d; cb += 32) {
+                for (int idx = tid; idx < kb * 32; idx += NT) {
+                    const int c = idx / kb, k = idx - c * kb;
+                    sU[k * 32 + c] = cb + c < d ? A[(long long)(cb + c) * d + k0 + k] : make_double2(0.0, 0.0);
+                }
+                __syncthreads();
+                double2 acc[2][4];
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int i = rb + lane + 32 * a, j = cb + 4 * warp + c;
+                        acc[a][c] = (i < d && j < d) ? A[(long long)j * d + i] : make_double2(0.0, 0.0);
+                    }
+                for (int k = 0; k < kb; ++k) {
+                    const double2 l0 = sL[k * LU_MB + lane], l1 = sL[k * LU_MB + lane + 32];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double2 u = sU[k * 32 + 4 * warp + c];
+                        acc[0][c] = make_double2(acc[0][c].x - (l0.x * u.x - l0.y * u.y),
+                                                 acc[0][c].y - (l0.x * u.y + l0.y * u.x));
+                        acc[1][c] = make_double2(acc[1][c].x - (l1.x * u.x - l1.y * u.y),
+                                                 acc[1][c].y - (l1.x * u.y + l1.y * u.x));
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int i = rb + lane + 32 * a, j = cb + 4 * warp + c;
+                        if (i < d && j < d) A[(long long)j * d + i] = acc[a][c];
+                    }
+                __syncthreads();
+            }
+        }
+    }
+}
+
 template <int NT>
 __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
                            int* __restrict__ rowat, int* __restrict__ pos, int* __restrict__ dflag,
-                           double2* __restrict__ dk, double hl0, double* s_pv, int* s_pi) {
+                           double2* __restrict__ dk, double hl0, double* s_pv, int* s_pi,
+                           double2* tiles) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = P.d;
@@ -134,31 +282,15 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         A[(long long)i * d + i].x += 1.0;
     }
     __syncthreads();
+    if constexpr (NT == 256) {
+        if (tiles) {
+            lu_blocked<NT>(A, ipiv, d, tiles, s_pv, s_pi);
+            goto lu_done;
+        }
+    }
     for (int k = 0; k < d; ++k) {
         double2* const ck = A + (long long)k * d;
-        // izamax over rows k..d-1: the first row of maximal |re| + |im|
-        double bv = -1.0;
-        int bi = d;
-        for (int i = k + tid; i < d; i += NT) {
-            const double2 a = ck[i];
-            const double v = fabs(a.x) + fabs(a.y);
-            if (v > bv) { bv = v; bi = i; }
-        }
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, m);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
-            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        if constexpr (NW > 1) {
-            if (lane == 0) { s_pv[warp] = bv; s_pi[warp] = bi; }
-            __syncthreads();
-            bv = s_pv[0];
-            bi = s_pi[0];
-            for (int w = 1; w < NW; ++w)
-                if (s_pv[w] > bv || (s_pv[w] == bv && s_pi[w] < bi)) { bv = s_pv[w]; bi = s_pi[w]; }
-        }
-        const int p = bi < d ? bi : k;
+        const int p = pivot_row<NT>(ck, k, d, s_pv, s_pi);
         if (tid == 0) ipiv[k] = p;
         const double2 piv = ck[p];
         __syncthreads();  // every thread holds the pivot before the rows move
@@ -183,6 +315,7 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         }
         __syncthreads();
     }
+lu_done:
     // Solve-side constants, computed once per factorisation: pos[i] = where
     // b[i] lands after zlaswp's sequential interchanges (the caller writes the
     // residual pre-permuted), and the divisor-only part of cdiv_np(x, U(k,k))
@@ -504,7 +637,8 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                     const double hl0 = h * l0;
                     if (!(has_lu && !jac_stale && fabs(hl0 / hl0_fact - 1.0) <= 0.3)) {
                         jac_stale = false;
-                        bdf_factor<NT>(P, A, IPIV, ROWAT, POS, DFLAG, DK, hl0, s_pv, s_pi);
+                        bdf_factor<NT>(P, A, IPIV, ROWAT, POS, DFLAG, DK, hl0, s_pv, s_pi,
+                                       B.in_smem ? nullptr : smem);
                         if (B.inverse) bdf_invert<NT>(d, A, IPIV, X);
                         st[sLuFactor]++;
                         has_lu = true;

@@ -666,9 +666,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
         // Newton solves: substitution with the LU (zgetrs) for small d, where
         // the matrix is refactored every few attempts; the explicit inverse
-        // (zgetri) from d = 48 up, where 2d barrier-separated substitution
-        // steps per solve dominate (c3 BDF: 2.5x; c2 (d = 20): 0.7x)
-        p->bdf_inverse = d->dim >= 48;
+        // (zgetri) for 48 <= d <= 256, where 2d barrier-separated substitution
+        // steps per solve dominate (c3 BDF: 2.5x; c2 (d = 20): 0.7x); above
+        // that the unblocked inversion would re-read the HBM matrix d times
+        p->bdf_inverse = d->dim >= 48 && d->dim <= 256;
         if (const char* ev = getenv("QTM_BDF_SOLVE")) p->bdf_inverse = strcmp(ev, "lu") != 0;
         if (const char* ev = getenv("QTM_BDF_THREADS")) {  // A/B experiments
             const int v = atoi(ev);
@@ -683,7 +684,8 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         const size_t bcap = (size_t)smem_cap > bstatic ? (size_t)smem_cap - bstatic : 0;
         const size_t bytes = sizeof(double2) * (size_t)p->bdf_ws_elems;
         p->bdf_in_smem = bytes <= bcap;
-        p->smem = p->bdf_in_smem ? bytes : 0;
+        // HBM workspace with 256 threads: the blocked LU's tiles in shared memory
+        p->smem = p->bdf_in_smem ? bytes : (p->bdf_threads == 256 ? sizeof(double2) * LU_TILE_ELEMS : 0);
         if (cudaFuncSetAttribute(p->bdf_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bcap) != cudaSuccess)
             rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem, BDF) failed");
     }
