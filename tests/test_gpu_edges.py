@@ -6,12 +6,12 @@ overflow scratch) -- each against the C oracle on identical streams."""
 import numpy as np
 import pytest
 
-from paper_1810_03047_b200.csr import tensor
+from paper_1810_03047_b200.csr import CsrMatrix
 from paper_1810_03047_b200.engine import DeviceProblem, run_gpu
 from paper_1810_03047_b200.packing import pack_problem
 from paper_1810_03047_b200.problem import OdeConfig, QuantumProblem, RunOptions
-from paper_1810_03047_b200.qops import (OperatorSet, coherent, destroy, eye, fock, sigma_minus,
-                                        sigma_x, sigma_z)
+from paper_1810_03047_b200.qops import (EffectiveGenerator, OperatorSet, coherent, destroy, fock,
+                                        sigma_minus, sigma_x, sigma_z)
 
 pytestmark = pytest.mark.gpu
 
@@ -67,20 +67,29 @@ def test_ragged_dimensions(n_fock, oracle_lib):
 def test_dimension_4096(oracle_lib):
     """12-site dissipative Ising chain: past every shared-memory staging
     (G read as CSR through L2, two history rows in registers)."""
-    n_sites = 12
+    import scipy.sparse as sp
+    n_sites, dim = 12, 2 ** 12
 
-    def site(op, i):
-        f = [eye(2)] * n_sites
-        f[i] = op
-        return tensor(*f)
+    def site(op, i):  # sparse kron, site 0 leftmost (linalg.py:111-118)
+        return sp.kron(sp.kron(sp.identity(2 ** i), sp.csr_matrix(op)),
+                       sp.identity(2 ** (n_sites - 1 - i)), format="csr")
+
+    def csr(m):
+        m = sp.csr_matrix(m, dtype=np.complex128)
+        m.eliminate_zeros()
+        m.sort_indices()
+        return CsrMatrix(dim, m.indptr.astype(np.int64), m.indices.astype(np.int64), m.data)
     sz = [site(sigma_z(), i) for i in range(n_sites)]
     h = sum(-1.0 * (sz[i] @ sz[i + 1]) for i in range(n_sites - 1))
     h = h + sum(-0.7 * site(sigma_x(), i) for i in range(n_sites))
-    ops = OperatorSet(h, tuple(np.sqrt(0.05) * site(sigma_minus(), i) for i in range(n_sites)),
-                      (sz[0], sz[n_sites // 2]))
-    p = QuantumProblem.from_operators(ops, fock(2 ** n_sites, 0), 0.0, 1.0, 10,
-                                      ode=OdeConfig(rtol=1e-8, atol=1e-10),
-                                      options=RunOptions(log_jumps=True))
+    cs = [np.sqrt(0.05) * site(sigma_minus(), i) for i in range(n_sites)]
+    g = -1j * h
+    for c in cs:
+        g = g - 0.5 * (c.conj().T @ c)
+    p = QuantumProblem(generator=EffectiveGenerator(csr(g)), collapse_csr=tuple(csr(c) for c in cs),
+                       expect_csr=(csr(sz[0]), csr(sz[n_sites // 2])), psi0=fock(dim, 0),
+                       t_from=0.0, t_to=4.0, n_steps=20, ode=OdeConfig(rtol=1e-8, atol=1e-10),
+                       options=RunOptions(log_jumps=True))
     pk = pack_problem(p)
     assert pk.dim == 4096
     _check(pk, 4, oracle_lib)
