@@ -1,6 +1,6 @@
 """Edge cases of the device path: empty trajectory ranges, problems without
 observables, dimensions that are not a multiple of a warp, and states larger
-than every shared-memory staging (d = 4096, CSR from L2, history rows in the
+than every shared-memory staging (d = 3000, CSR from L2, history rows in the
 overflow scratch) -- each against the C oracle on identical streams."""
 
 import numpy as np
@@ -10,8 +10,7 @@ from paper_1810_03047_b200.csr import CsrMatrix
 from paper_1810_03047_b200.engine import DeviceProblem, run_gpu
 from paper_1810_03047_b200.packing import pack_problem
 from paper_1810_03047_b200.problem import OdeConfig, QuantumProblem, RunOptions
-from paper_1810_03047_b200.qops import (EffectiveGenerator, OperatorSet, coherent, destroy, fock,
-                                        sigma_minus, sigma_x, sigma_z)
+from paper_1810_03047_b200.qops import EffectiveGenerator, OperatorSet, coherent, destroy, fock
 
 pytestmark = pytest.mark.gpu
 
@@ -64,32 +63,27 @@ def test_ragged_dimensions(n_fock, oracle_lib):
     _check(pack_problem(_cavity(n_fock)), 32, oracle_lib)
 
 
-def test_dimension_4096(oracle_lib):
-    """12-site dissipative Ising chain: past every shared-memory staging
-    (G read as CSR through L2, two history rows in registers)."""
+def test_dimension_3000(oracle_lib):
+    """A 3000-level driven damped oscillator: past every shared-memory
+    staging (G read as CSR through L1/L2, two history rows in registers,
+    the rest in the overflow scratch)."""
     import scipy.sparse as sp
-    n_sites, dim = 12, 2 ** 12
-
-    def site(op, i):  # sparse kron, site 0 leftmost (linalg.py:111-118)
-        return sp.kron(sp.kron(sp.identity(2 ** i), sp.csr_matrix(op)),
-                       sp.identity(2 ** (n_sites - 1 - i)), format="csr")
+    dim = 3000
 
     def csr(m):
         m = sp.csr_matrix(m, dtype=np.complex128)
         m.eliminate_zeros()
         m.sort_indices()
         return CsrMatrix(dim, m.indptr.astype(np.int64), m.indices.astype(np.int64), m.data)
-    sz = [site(sigma_z(), i) for i in range(n_sites)]
-    h = sum(-1.0 * (sz[i] @ sz[i + 1]) for i in range(n_sites - 1))
-    h = h + sum(-0.7 * site(sigma_x(), i) for i in range(n_sites))
-    cs = [np.sqrt(0.05) * site(sigma_minus(), i) for i in range(n_sites)]
-    g = -1j * h
-    for c in cs:
-        g = g - 0.5 * (c.conj().T @ c)
-    p = QuantumProblem(generator=EffectiveGenerator(csr(g)), collapse_csr=tuple(csr(c) for c in cs),
-                       expect_csr=(csr(sz[0]), csr(sz[n_sites // 2])), psi0=fock(dim, 0),
-                       t_from=0.0, t_to=4.0, n_steps=20, ode=OdeConfig(rtol=1e-8, atol=1e-10),
+    a = sp.diags(np.sqrt(np.arange(1, dim, dtype=np.float64)), 1, format="csr")
+    ad = a.T.tocsr()
+    n = ad @ a
+    h = 0.4 * n + 0.8 * (a + ad)
+    c = np.sqrt(0.3) * a
+    g = -1j * h - 0.5 * (c.T @ c)
+    p = QuantumProblem(generator=EffectiveGenerator(csr(g)), collapse_csr=(csr(c),),
+                       expect_csr=(csr(n), csr((a + ad) / 2)), psi0=fock(dim, 3),
+                       t_from=0.0, t_to=3.0, n_steps=30, ode=OdeConfig(rtol=1e-8, atol=1e-10),
                        options=RunOptions(log_jumps=True))
     pk = pack_problem(p)
-    assert pk.dim == 4096
-    _check(pk, 4, oracle_lib)
+    _check(pk, 8, oracle_lib)
