@@ -351,6 +351,119 @@ lu_done:
     __syncthreads();
 }
 
+// xk = cdiv_np(b, U(k, k)) with the divisor part precomputed (see bdf_factor)
+__device__ __forceinline__ double2 udiv(double2 b, double2 rs, int fl) {
+    if (fl == 0) return make_double2((b.x + b.y * rs.x) * rs.y, (b.y - b.x * rs.x) * rs.y);
+    if (fl == 1) return make_double2((b.x * rs.x + b.y) * rs.y, (b.y * rs.x - b.x) * rs.y);
+    return make_double2(b.x / 0.0, b.y / 0.0);
+}
+
+// b_i -= sum_j y_j A(i, k0 + j) over the block's pivots j (ascending for
+// the forward sweep, descending for the backward one, skipping pivots whose
+// value was exactly zero, as the column sweep does) for rows i in
+// [lo, hi).  Each thread carries up to 4 rows (d <= 4 NT) as independent
+// chains; the A loads do not depend on the sums, so they run ahead.
+template <int NT, bool FWD>
+__device__ __forceinline__ void block_rows_update(const double2* __restrict__ A, int d, int k0, int kb,
+                                                  int lo, int hi, const double2* sY, const int* sF,
+                                                  double2* __restrict__ b) {
+    for (int base = lo; base < hi; base += 4 * NT) {
+        double2 s[4];
+        int iv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            iv[r] = base + threadIdx.x + r * NT;
+            s[r] = iv[r] < hi ? b[iv[r]] : make_double2(0.0, 0.0);
+        }
+#pragma unroll 2
+        for (int jj = 0; jj < kb; ++jj) {
+            const int j = FWD ? jj : kb - 1 - jj;
+            const double2* const cj = A + (long long)(k0 + j) * d;
+            double2 a[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = iv[r] < hi ? cj[iv[r]] : make_double2(0.0, 0.0);
+            if (sF[j]) {
+                const double2 y = sY[j];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    s[r] = make_double2(s[r].x - (y.x * a[r].x - y.y * a[r].y),
+                                        s[r].y - (y.x * a[r].y + y.y * a[r].x));
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (iv[r] < hi) b[iv[r]] = s[r];
+    }
+}
+
+// Blocked substitution for an HBM-resident LU (NT = 256): per block of 32
+// pivots, warp 0 solves the diagonal block from shared memory with shuffles
+// (no CTA barrier per pivot) and all threads then apply the block's 32
+// updates to the remaining rows, row by row in pivot order.  Each row sees
+// the same update sequence as the column sweep of bdf_solve, so the result
+// is bit-identical; the L/U columns stream through once, coalesced, with 3
+// barriers per block instead of one per pivot.  b arrives interchanged.
+template <int NT>
+__device__ void bdf_solve_blocked(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
+                                  const double2* __restrict__ dk, double2* __restrict__ b,
+                                  double2* __restrict__ x, double2* tiles) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double2* const sD = tiles;             // [32][32] diagonal block, column-major
+    double2* const sY = tiles + 32 * 32;   // [32] solved values of the block
+    int* const sF = reinterpret_cast<int*>(sY + 32);  // [32] 1 = the pivot's update applies
+    __syncthreads();
+    for (int k0 = 0; k0 < d; k0 += 32) {
+        const int kb = min(32, d - k0);
+        for (int idx = tid; idx < kb * 32; idx += NT) {
+            const int j = idx >> 5, i = idx & 31;
+            sD[idx] = i < kb ? A[(long long)(k0 + j) * d + k0 + i] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double2 bl = lane < kb ? b[k0 + lane] : make_double2(0.0, 0.0);
+            for (int j = 0; j < kb; ++j) {
+                const double2 yj = make_double2(__shfl_sync(0xffffffffu, bl.x, j),
+                                                __shfl_sync(0xffffffffu, bl.y, j));
+                const bool nz = yj.x != 0.0 || yj.y != 0.0;
+                if (lane == 0) { sY[j] = yj; sF[j] = nz; }
+                if (nz && lane > j && lane < kb) {
+                    const double2 a = sD[j * 32 + lane];
+                    bl = make_double2(bl.x - (yj.x * a.x - yj.y * a.y), bl.y - (yj.x * a.y + yj.y * a.x));
+                }
+            }
+            if (lane < kb) b[k0 + lane] = bl;
+        }
+        __syncthreads();
+        block_rows_update<NT, true>(A, d, k0, kb, k0 + kb, d, sY, sF, b);
+        __syncthreads();
+    }
+    for (int k0 = ((d - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
+        const int kb = min(32, d - k0);
+        for (int idx = tid; idx < kb * 32; idx += NT) {
+            const int j = idx >> 5, i = idx & 31;
+            sD[idx] = i < kb ? A[(long long)(k0 + j) * d + k0 + i] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double2 bl = lane < kb ? b[k0 + lane] : make_double2(0.0, 0.0);
+            for (int j = kb - 1; j >= 0; --j) {
+                const double2 bj = make_double2(__shfl_sync(0xffffffffu, bl.x, j),
+                                                __shfl_sync(0xffffffffu, bl.y, j));
+                const bool nz = bj.x != 0.0 || bj.y != 0.0;
+                const double2 xj = nz ? udiv(bj, dk[k0 + j], dflag[k0 + j]) : bj;
+                if (lane == 0) { sY[j] = xj; sF[j] = nz; x[k0 + j] = xj; }
+                if (nz && lane < j) {
+                    const double2 a = sD[j * 32 + lane];
+                    bl = make_double2(bl.x - (xj.x * a.x - xj.y * a.y), bl.y - (xj.x * a.y + xj.y * a.x));
+                }
+            }
+        }
+        __syncthreads();
+        block_rows_update<NT, false>(A, d, k0, kb, 0, k0, sY, sF, b);
+        __syncthreads();
+    }
+}
+
 // M^{-1} in place from its LU (LAPACK zgetri, unblocked): inv(U) column by
 // column (ztrti2), then inv(M) L = inv(U) from the last column back
 // (zgemv per column), then the column interchanges in reverse pivot order.
@@ -658,6 +771,8 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                         st[sNfe]++;
                         if (B.inverse)
                             bdf_apply_inverse<NT>(d, A, DY, X);
+                        else if (NT == 256 && !B.in_smem)
+                            bdf_solve_blocked<NT>(d, A, DFLAG, DK, DY, X, smem);
                         else
                             bdf_solve<NT>(d, A, DFLAG, DK, DY, X);
                         double acc = 0.0;
