@@ -319,8 +319,24 @@ def main_td():
     print(f"td fixtures done in {time.time() - t0:.1f}s")
 
 
+def main_lindblad():
+    """Ensemble limits (``lindblad_*.npz``): the reference's dense Lindblad
+    oracle ``solve_master_equation`` (trajectory.py:276-299) on c1 and c2 --
+    what the trajectory average converges to as N grows."""
+    from mcwf.trajectory import solve_master_equation
+    t0 = time.time()
+    for name, build in (("c1", ref_configs.c1_ops), ("c2", ref_configs.c2_ops)):
+        ops, psi0, times = build()
+        rho0 = np.outer(psi0, psi0.conj())
+        vals = solve_master_equation(ops, rho0, times, ode=OdeConfig(rtol=1e-8, atol=1e-10))
+        np.savez_compressed(os.path.join(HERE, f"lindblad_{name}.npz"), times=times, values=vals)
+        print(f"  lindblad_{name}: {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    if "--td" in sys.argv:
+    if "--lindblad" in sys.argv:
+        main_lindblad()
+    elif "--td" in sys.argv:
         main_td()
     elif "--bdf" in sys.argv:
         main_bdf()

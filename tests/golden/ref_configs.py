@@ -30,18 +30,28 @@ def _problem(ops, psi0, t_to, n_steps, log_jumps):
                                          options=RunOptions(log_jumps=log_jumps))
 
 
-def c1(log_jumps=True):
+def c1_ops():
     sm = sigma_minus()
     ops = OperatorSet(0.5 * sigma_x(), (sqrt(0.1) * sm,), (sigma_z(), dagger(sm) @ sm))
-    return _problem(ops, fock(2, 0), 20.0, 200, log_jumps)
+    return ops, fock(2, 0), __import__("numpy").linspace(0.0, 20.0, 201)
 
 
-def c2(log_jumps=True):
+def c1(log_jumps=True):
+    ops, psi0, _ = c1_ops()
+    return _problem(ops, psi0, 20.0, 200, log_jumps)
+
+
+def c2_ops():
     a = destroy(20)
     ad = dagger(a)
     ops = OperatorSet(0.5 * (ad @ a) + 1.0 * (a + ad), (sqrt(0.5) * a,),
                       (ad @ a, (a + ad) / 2))
-    return _problem(ops, coherent(20, 2.0), 30.0, 300, log_jumps)
+    return ops, coherent(20, 2.0), __import__("numpy").linspace(0.0, 30.0, 301)
+
+
+def c2(log_jumps=True):
+    ops, psi0, _ = c2_ops()
+    return _problem(ops, psi0, 30.0, 300, log_jumps)
 
 
 def c3(log_jumps=True):

@@ -305,3 +305,22 @@ def test_shared_memory_history_variants_agree(name):
     assert a.rc == 0 and b.rc == 0
     np.testing.assert_array_equal(a.jump_count, b.jump_count)
     np.testing.assert_allclose(a.values, b.values, rtol=0, atol=TOL)
+
+
+@pytest.mark.parametrize("name,n,method", [("c1", 100_000, "adams"), ("c2", 5000, "adams"),
+                                           ("c2", 5000, "bdf")])
+def test_ensemble_converges_to_lindblad(name, n, method):
+    """Device ensembles vs the reference's dense master-equation oracle
+    (tests/golden/lindblad_<name>.npz): within 4.5 SE at every grid point."""
+    import dataclasses
+    import os
+    z = np.load(os.path.join(goldens.GOLDEN_DIR, f"lindblad_{name}.npz"))
+    p = configs.build(name)
+    if method == "bdf":
+        p = dataclasses.replace(p, ode=OdeConfig(method="bdf", rtol=p.ode.rtol, atol=p.ode.atol))
+    with DeviceProblem(p) as dp:
+        out = dp.run(4242, 0, n, per_trajectory=False, resident=True)
+    assert out.rc == 0
+    mean = out.sum / n
+    se = np.sqrt(np.maximum(out.sumsq / n - mean ** 2, 0) * n / (n - 1) / n)
+    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-6)

@@ -136,3 +136,20 @@ def test_time_dependent_generator_call_order():
         import dataclasses
         from paper_1810_03047_b200.problem import OdeConfig
         pack_problem(dataclasses.replace(g.problem, ode=OdeConfig(method="bdf")))
+
+
+# ---- ensemble limit: the unravelling converges to the Lindblad solution ------
+@pytest.mark.parametrize("name,n", [("c1", 4000), ("c2", 600)])
+def test_oracle_ensemble_converges_to_lindblad(name, n, oracle_lib):
+    """The trajectory average vs the reference's dense master-equation
+    oracle (solve_master_equation, trajectory.py:276-299; fixture
+    tests/golden/lindblad_<name>.npz): within 4.5 standard errors at every
+    point, plus the ODE tolerance."""
+    import os
+    from paper_1810_03047_b200 import configs
+    z = np.load(os.path.join(goldens.GOLDEN_DIR, f"lindblad_{name}.npz"))
+    r = oracle_lib.run(pack_problem(configs.build(name)), 2024, 0, n)
+    mean = r["values"].mean(axis=0)
+    se = r["values"].std(axis=0, ddof=1) / np.sqrt(n)
+    np.testing.assert_allclose(z["times"], configs.build(name).time_grid(), rtol=0, atol=1e-12)
+    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-6)
