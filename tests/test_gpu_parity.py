@@ -323,4 +323,6 @@ def test_ensemble_converges_to_lindblad(name, n, method):
     assert out.rc == 0
     mean = out.sum / n
     se = np.sqrt(np.maximum(out.sumsq / n - mean ** 2, 0) * n / (n - 1) / n)
-    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-6)
+    # (+1e-3: before the first jumps of a finite ensemble its sample SE is 0
+    # while the Lindblad curve already carries the O(t) jump probability)
+    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-3)

@@ -152,4 +152,6 @@ def test_oracle_ensemble_converges_to_lindblad(name, n, oracle_lib):
     mean = r["values"].mean(axis=0)
     se = r["values"].std(axis=0, ddof=1) / np.sqrt(n)
     np.testing.assert_allclose(z["times"], configs.build(name).time_grid(), rtol=0, atol=1e-12)
-    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-6)
+    # (+1e-3: before the first jumps of a finite ensemble its sample SE is 0
+    # while the Lindblad curve already carries the O(t) jump probability)
+    assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-3)
