@@ -371,7 +371,7 @@ def main(argv=None):
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             hbm_peak = float(json.load(f)["hbm_gbs"])
     except (OSError, KeyError, ValueError):
-        hbm_peak = 7700.0  # B200_PROFILING.md fallback
+        hbm_peak = 6650.0  # B200_PROFILING.md fallback ("of fallback")
     layout = dp.layout()
     dp.close()
 
