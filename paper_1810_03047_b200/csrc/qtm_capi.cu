@@ -107,6 +107,20 @@ __global__ void stats_total(const long long* __restrict__ stats, const int* __re
 namespace {
 
 thread_local std::string g_last_error;
+
+// Pinned host staging for a call's results (control words, counters,
+// per-point sums): the device->host copies stay asynchronous, so a call
+// synchronises its stream once.  One buffer per host thread, grown on
+// demand and kept for the thread's lifetime (pinning is expensive; calls on
+// different threads never share it).
+struct PinnedStage {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedStage() {
+        if (p) cudaFreeHost(p);
+    }
+};
+thread_local PinnedStage g_stage;
 unsigned long long g_phase_cycles[16];  // last run's phase counters (QTM_PHASES builds)
 
 int set_error(int code, const std::string& msg) {
@@ -811,6 +825,20 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         CUDA_TRY(cudaMemcpyAsync(p->script_len.p, a->script_len, sizeof(int64_t) * count,
                                  cudaMemcpyHostToDevice, s));
     }
+    const size_t pin_bytes = sizeof(unsigned long long) * 18 + sizeof(long long) * (QTM_NSTATS + 1) +
+                             sizeof(double) * 2 * (size_t)std::max(n_out, 1);
+    if (g_stage.bytes < pin_bytes) {
+        if (g_stage.p) cudaFreeHost(g_stage.p);
+        g_stage.p = nullptr;
+        g_stage.bytes = 0;
+        const size_t want = std::max<size_t>(pin_bytes, 1 << 16);
+        CUDA_TRY(cudaMallocHost(&g_stage.p, want));
+        g_stage.bytes = want;
+    }
+    unsigned long long* const h_ctl = static_cast<unsigned long long*>(g_stage.p);
+    long long* const h_tot = reinterpret_cast<long long*>(h_ctl + 18);
+    double* const h_sum = reinterpret_cast<double*>(h_tot + QTM_NSTATS + 1);
+    double* const h_sumsq = h_sum + std::max(n_out, 1);
     CUDA_TRY(cudaEventRecord(p->ev[0], s));
     long long totals[QTM_NSTATS + 1] = {0};
     int64_t launches = 0;
@@ -822,8 +850,9 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     for (long long off = 0; off < count; off += kRunChunk) {
         const long long cnt = std::min<long long>(kRunChunk, count - off);
         const long long cgrid = std::min<long long>(grid, cnt);
-        unsigned long long ctl_init[18] = {0ull, ~0ull};
-        CUDA_TRY(cudaMemcpyAsync(p->ctl.p, ctl_init, sizeof(ctl_init), cudaMemcpyHostToDevice, s));
+        // ctl = {work counter 0, first failing row ~0, phase counters 0}
+        CUDA_TRY(cudaMemsetAsync(p->ctl.p, 0, sizeof(unsigned long long) * 18, s));
+        CUDA_TRY(cudaMemsetAsync(p->ctl.p + 1, 0xFF, sizeof(unsigned long long), s));
         RunParams R{};
         R.seed = a->seed;
         R.traj_begin = a->traj_begin + off;
@@ -870,10 +899,10 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         stats_total<<<1, 32, 0, s>>>(p->stats.p, p->status.p, cnt, p->stats_tot.p);
         launches += 1 + 1 + (n_out > 0 ? 1 : 0) + 1;
         CUDA_TRY(cudaGetLastError());
-        unsigned long long ctl_out[18];
-        long long tot_host[QTM_NSTATS + 1];
-        CUDA_TRY(cudaMemcpyAsync(ctl_out, p->ctl.p, sizeof(ctl_out), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(tot_host, p->stats_tot.p, sizeof(tot_host), cudaMemcpyDeviceToHost, s));
+        const bool last = off + kRunChunk >= count;
+        CUDA_TRY(cudaMemcpyAsync(h_ctl, p->ctl.p, sizeof(unsigned long long) * 18, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(h_tot, p->stats_tot.p, sizeof(long long) * (QTM_NSTATS + 1),
+                                 cudaMemcpyDeviceToHost, s));
         if (copy_per_traj) {
             if (o->values && n_out > 0)
                 CUDA_TRY(cudaMemcpyAsync(o->values + off * n_out, p->values.p, sizeof(double) * cnt * n_out,
@@ -893,7 +922,22 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
                 CUDA_TRY(cudaMemcpyAsync(o->jump_idx + off * max_jumps, p->jump_idx.p,
                                          sizeof(int32_t) * cnt * max_jumps, cudaMemcpyDeviceToHost, s));
         }
+        if (last) {
+            if (n_out > 0) {
+                ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, (int)n_red_total, n_out,
+                                                                   p->sum.p, p->sumsq.p);
+                launches += 1;
+                CUDA_TRY(cudaGetLastError());
+                CUDA_TRY(cudaMemcpyAsync(h_sum, p->sum.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(h_sumsq, p->sumsq.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
+            }
+            CUDA_TRY(cudaEventRecord(p->ev[3], s));
+        }
         CUDA_TRY(cudaStreamSynchronize(s));
+        unsigned long long ctl_out[18];
+        long long tot_host[QTM_NSTATS + 1];
+        memcpy(ctl_out, h_ctl, sizeof(ctl_out));
+        memcpy(tot_host, h_tot, sizeof(tot_host));
         float ms = 0.f;
         cudaEventElapsedTime(&ms, p->ev[1], p->ev[2]);
         kernel_ms += ms;
@@ -919,15 +963,9 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         }
     }
     if (n_out > 0) {
-        ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, (int)n_red_total, n_out,
-                                                           p->sum.p, p->sumsq.p);
-        launches += 1;
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaMemcpyAsync(o->sum, p->sum.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
-        if (o->sumsq) CUDA_TRY(cudaMemcpyAsync(o->sumsq, p->sumsq.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, s));
+        memcpy(o->sum, h_sum, sizeof(double) * n_out);
+        if (o->sumsq) memcpy(o->sumsq, h_sumsq, sizeof(double) * n_out);
     }
-    CUDA_TRY(cudaEventRecord(p->ev[3], s));
-    CUDA_TRY(cudaStreamSynchronize(s));
     cudaEventElapsedTime(&o->total_ms, p->ev[0], p->ev[3]);
     o->kernel_ms = kernel_ms;
     o->launches = launches;
