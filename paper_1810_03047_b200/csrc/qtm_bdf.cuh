@@ -282,13 +282,14 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         A[(long long)i * d + i].x += 1.0;
     }
     __syncthreads();
+    bool blocked = false;
     if constexpr (NT == 256) {
         if (tiles) {
             lu_blocked<NT>(A, ipiv, d, tiles, s_pv, s_pi);
-            goto lu_done;
+            blocked = true;
         }
     }
-    for (int k = 0; k < d; ++k) {
+    for (int k = 0; k < d && !blocked; ++k) {
         double2* const ck = A + (long long)k * d;
         const int p = pivot_row<NT>(ck, k, d, s_pv, s_pi);
         if (tid == 0) ipiv[k] = p;
@@ -315,7 +316,6 @@ __device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __
         }
         __syncthreads();
     }
-lu_done:
     // Solve-side constants, computed once per factorisation: pos[i] = where
     // b[i] lands after zlaswp's sequential interchanges (the caller writes the
     // residual pre-permuted), and the divisor-only part of cdiv_np(x, U(k,k))
@@ -355,7 +355,7 @@ lu_done:
 __device__ __forceinline__ double2 udiv(double2 b, double2 rs, int fl) {
     if (fl == 0) return make_double2((b.x + b.y * rs.x) * rs.y, (b.y - b.x * rs.x) * rs.y);
     if (fl == 1) return make_double2((b.x * rs.x + b.y) * rs.y, (b.y * rs.x - b.x) * rs.y);
-    return make_double2(b.x / 0.0, b.y / 0.0);
+    return make_double2(b.x / rs.y, b.y / rs.y);  // U(k, k) = 0: rs = (0, 0), numpy's b / 0
 }
 
 // b_i -= sum_j y_j A(i, k0 + j) over the block's pivots j (ascending for
@@ -572,12 +572,7 @@ __device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __res
             // xk = cdiv_np(b[k], U(k, k)) with the divisor part precomputed
             const double2 rs = dk[k];
             const int fl = dflag[k];
-            if (fl == 0)
-                xk = make_double2((xk.x + xk.y * rs.x) * rs.y, (xk.y - xk.x * rs.x) * rs.y);
-            else if (fl == 1)
-                xk = make_double2((xk.x * rs.x + xk.y) * rs.y, (xk.y * rs.x - xk.x) * rs.y);
-            else
-                xk = make_double2(xk.x / 0.0, xk.y / 0.0);
+            xk = udiv(xk, rs, fl);
             const double2* const ck = A + (long long)k * d;
             for (int i = tid; i < k; i += NT) {
                 const double2 a = ck[i], bi = b[i];
