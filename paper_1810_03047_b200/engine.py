@@ -6,8 +6,9 @@ the return type of the reference's ``run_inline``
 0..n_total-1, averages ⟨E_k⟩(t_j) over them and returns a
 ``TrajectoryResult``.  The per-trajectory work (run_single_trajectory,
 trajectory.py:190-250, and the solver it drives, ode.py) runs inside one
-persistent sm_100a kernel per call (csrc/qtm_traj.cuh) behind the C ABI in
-include/qtm.h.
+persistent sm_100a kernel per call behind the C ABI in include/qtm.h:
+csrc/qtm_traj.cuh for the ADAMS family (constant generator, or a
+TimeDependentGenerator rhs_fn, timedep.py), csrc/qtm_bdf.cuh for BDF.
 
 Random streams are per trajectory and keyed by the global index (see
 csrc/qtm_rng.cuh), so the ensemble does not depend on how it is sharded
