@@ -283,26 +283,29 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
 // Sliced-ELL copy of G for shared-memory staging (see DevProblem::sell_*).
 // Returns false (and leaves sell_mode = 0) when the operator cannot be
 // encoded (dimension > 4096 or > 4095 distinct values) or the staged copy
-// does not fit next to the kernel's fixed shared memory.  With `td1` (a TD
-// variant, one time-dependent term G1) the slots follow the union pattern of
-// G0 and G1 and a uint16 array gives G1's value per slot (sell_td_*); if
-// that does not fit, G0 alone is staged and G1 stays in L2 (row_dot).
+// does not fit next to the kernel's fixed shared memory.  With `tds` (a TD
+// variant's time-dependent terms G_k) the slots follow the union pattern of
+// G0 and every G_k and one uint16 array per term gives G_k's value per slot
+// (sell_td_*); if that does not fit, G0 alone is staged and the G_k stay in
+// L2 (row_dot).
 int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
-               size_t smem_cap, bool* staged, const qtm_csr* td1 = nullptr) {
+               size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {}) {
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
     if (n > 4096) return QTM_OK;  // byte offsets col*16 must fit 16 bits
-    for (int pass = td1 ? 0 : 1; pass < 2; ++pass) {
-        const qtm_csr* t1 = pass == 0 ? td1 : nullptr;
+    for (int pass = tds.empty() ? 1 : 0; pass < 2; ++pass) {
+        const int nt1 = pass == 0 ? (int)tds.size() : 0;
         // per row: the union of G0's and G1's columns, ascending
         std::vector<std::vector<int64_t>> cols(n);
         std::vector<int> width(nslices, 0);
         for (int64_t i = 0; i < n; ++i) {
             std::vector<int64_t>& c = cols[i];
             for (int64_t j = g.row_ptr[i]; j < g.row_ptr[i + 1]; ++j) c.push_back(g.col_ind[j]);
-            if (t1) {
-                for (int64_t j = t1->row_ptr[i]; j < t1->row_ptr[i + 1]; ++j) c.push_back(t1->col_ind[j]);
+            if (nt1) {
+                for (int t = 0; t < nt1; ++t)
+                    for (int64_t j = tds[t]->row_ptr[i]; j < tds[t]->row_ptr[i + 1]; ++j)
+                        c.push_back(tds[t]->col_ind[j]);
                 std::sort(c.begin(), c.end());
                 c.erase(std::unique(c.begin(), c.end()), c.end());
             }
@@ -339,33 +342,39 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         std::vector<double2> dict(1, make_double2(0.0, 0.0)), tdict(1, make_double2(0.0, 0.0));
         std::map<Key, int> index, tindex;
         std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: x[0] * dict[0] (= 0)
-        std::vector<uint16_t> tent(t1 ? std::max(total, 1) : 0, 0);
+        const size_t nslot = (size_t)std::max(total, 1);
+        std::vector<uint16_t> tent((size_t)nt1 * nslot, 0);
         bool ok = true;
         for (int64_t i = 0; i < n && ok; ++i) {
             const int sl = (int)(i / 32), lane = (int)(i % 32);
-            int64_t j0 = g.row_ptr[i], j1 = t1 ? t1->row_ptr[i] : 0;
-            for (size_t k = 0; k < cols[i].size(); ++k) {
+            int64_t j0 = g.row_ptr[i];
+            std::vector<int64_t> jt(nt1);
+            for (int t = 0; t < nt1; ++t) jt[t] = tds[t]->row_ptr[i];
+            for (size_t k = 0; k < cols[i].size() && ok; ++k) {
                 const int64_t c = cols[i][k];
-                int vi = 0, ti = 0;
+                int vi = 0;  // a G_k-only slot: G0 contributes an exact zero
                 if (j0 < g.row_ptr[i + 1] && g.col_ind[j0] == c) {
                     vi = lookup(index, dict, g.values[2 * j0], g.values[2 * j0 + 1]);
                     ++j0;
-                } else {
-                    vi = 0;  // a G1-only slot: G0 contributes an exact zero
                 }
-                if (t1 && j1 < t1->row_ptr[i + 1] && t1->col_ind[j1] == c) {
-                    ti = lookup(tindex, tdict, t1->values[2 * j1], t1->values[2 * j1 + 1]);
-                    ++j1;
-                }
-                if (vi < 0 || ti < 0) { ok = false; break; }
+                if (vi < 0) { ok = false; break; }
                 const size_t slot = (size_t)off[sl] + k * 32 + lane;
                 ent[slot] = (uint32_t)(16 * c) | ((uint32_t)(16 * vi) << 16);
-                if (t1) tent[slot] = (uint16_t)(16 * ti);
+                for (int t = 0; t < nt1; ++t) {
+                    const qtm_csr* m = tds[t];
+                    int ti = 0;
+                    if (jt[t] < m->row_ptr[i + 1] && m->col_ind[jt[t]] == c) {
+                        ti = lookup(tindex, tdict, m->values[2 * jt[t]], m->values[2 * jt[t] + 1]);
+                        ++jt[t];
+                    }
+                    if (ti < 0) { ok = false; break; }
+                    tent[(size_t)t * nslot + slot] = (uint16_t)(16 * ti);
+                }
             }
         }
         if (!ok) continue;
         size_t bytes = sizeof(double2) * dict.size() + sizeof(uint32_t) * ent.size();
-        if (t1) bytes += sizeof(double2) * tdict.size() + sizeof(uint16_t) * tent.size();
+        if (nt1) bytes += sizeof(double2) * tdict.size() + sizeof(uint16_t) * tent.size();
         if (fixed_smem + bytes > smem_cap) continue;
         uint32_t* d_ent = nullptr;
         double2* d_dict = nullptr;
@@ -384,12 +393,12 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         P.sell_w = d_w;
         P.sell_td = 0;
         P.sell_td_dict_n = 0;
-        if (t1) {
+        if (nt1) {
             double2* d_tdict = nullptr;
             uint16_t* d_tent = nullptr;
             CUDA_TRY(upload(p, &d_tdict, tdict.data(), tdict.size()));
             CUDA_TRY(upload(p, &d_tent, tent.data(), tent.size()));
-            P.sell_td = 1;
+            P.sell_td = nt1;
             P.sell_td_dict_n = (int)tdict.size();
             P.sell_td_dict = d_tdict;
             P.sell_td_ent = d_tent;
@@ -705,8 +714,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     }
     if (rc == QTM_OK && p->method == 0) {
         bool staged = false;
-        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged,
-                        var.td && d->n_td == 1 ? &d->td[0] : nullptr);
+        std::vector<const qtm_csr*> tds;
+        if (var.td)
+            for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
+        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds);
     }
     if (rc == QTM_OK && p->method == 0) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");

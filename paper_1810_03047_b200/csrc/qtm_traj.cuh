@@ -84,10 +84,10 @@ struct DevProblem {
     const double2* sell_dict;
     const int* sell_off;    // [DP/32] first entry of each slice
     const int* sell_w;      // [DP/32] width of each slice
-    // TD variants with one time-dependent term: the SELL above is built on
-    // the union pattern of G0 and G1, and sell_td_ent (uint16 per slot, same
-    // slot layout) holds the byte offset of G1's value in sell_td_dict
-    // (offset 0 = 0.0); both staged after the G0 entries
+    // TD variants: the SELL above is built on the union pattern of G0 and
+    // the sell_td staged time-dependent terms, and sell_td_ent ([sell_td]
+    // arrays of uint16 per slot, same slot layout) holds the byte offset of
+    // G_k's value in sell_td_dict (offset 0 = 0.0); staged after the G0 entries
     int sell_td, sell_td_dict_n;
     const double2* sell_td_dict;
     const uint16_t* sell_td_ent;
@@ -324,6 +324,32 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
         out0[e] = make_double2(sr[e], si[e]);
         out1[e] = make_double2(tr[e], ti[e]);
     }
+}
+
+// G_k x alone over the union-pattern SELL (TD variants with several staged
+// terms): G_k's value per slot from its uint16 offsets, rows in column order.
+template <int NT, int E>
+__device__ __forceinline__ void sell_spmv_term(const uint32_t* __restrict__ ent, const uint16_t* __restrict__ tent,
+                                               const double2* __restrict__ tdict, const int (&off)[E], int width,
+                                               const double2* __restrict__ x, double2 (&out)[E]) {
+    const int lane = threadIdx.x & 31;
+    const char* const xb = reinterpret_cast<const char*>(x);
+    const char* const tb = reinterpret_cast<const char*>(tdict);
+    double tr[E], ti[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { tr[e] = 0.0; ti[e] = 0.0; }
+    for (int k = 0; k < width; ++k) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int slot = off[e] + k * 32 + lane;
+            const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
+            const double2 xv = *reinterpret_cast<const double2*>(xb + (ent[slot] & 0xFFFFu));
+            tr[e] = tr[e] + (w.x * xv.x - w.y * xv.y);
+            ti[e] = ti[e] + (w.x * xv.y + w.y * xv.x);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] = make_double2(tr[e], ti[e]);
 }
 
 // One lane-halving level of a multi-value warp reduction: lanes with bit m
@@ -827,7 +853,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
         if (TD && P.sell_td) {
             for (int i = tid; i < P.sell_td_dict_n; i += NT) s_tdict[i] = P.sell_td_dict[i];
-            for (int i = tid; i < P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
+            for (int i = tid; i < P.sell_td * P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
         }
         const int warp = tid >> 5;
 #pragma unroll
@@ -841,12 +867,24 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV_T(xs, f, tt)                                                   \
     do {                                                                     \
         if constexpr (TD) {                                                  \
-            if (P.sell_td) {                                                 \
+            if (P.sell_td == 1) {                                            \
                 double2 g__[E];                                              \
                 sell_spmv_td<NT, E>(s_ent, s_dict, s_tent, s_tdict, goff, gwidth, (xs), f, g__); \
                 const double c__ = td_coef(P, 0, (tt));                      \
                 _Pragma("unroll") for (int e = 0; e < E; ++e)                \
                     f[e] = make_double2(f[e].x + c__ * g__[e].x, f[e].y + c__ * g__[e].y); \
+                break;                                                       \
+            }                                                                \
+            if (P.sell_td > 1) {                                             \
+                GSPMV(xs, f);                                                \
+                for (int k__ = 0; k__ < P.sell_td; ++k__) {                  \
+                    double2 g__[E];                                          \
+                    sell_spmv_term<NT, E>(s_ent, s_tent + k__ * P.sell_entries, s_tdict, goff, \
+                                          gwidth, (xs), g__);                \
+                    const double c__ = td_coef(P, k__, (tt));                \
+                    _Pragma("unroll") for (int e = 0; e < E; ++e)            \
+                        f[e] = make_double2(f[e].x + c__ * g__[e].x, f[e].y + c__ * g__[e].y); \
+                }                                                            \
                 break;                                                       \
             }                                                                \
         }                                                                    \

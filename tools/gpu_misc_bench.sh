@@ -1,5 +1,4 @@
 #!/bin/bash
 cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_bdf.py -q -x -p no:cacheprovider > gpurun_out/misc_tests.log 2>&1; echo "rc=$?" >> gpurun_out/misc_tests.log
-timeout 900 python bench.py --config c4 --method bdf --trajectories 148 --steps 1 --warmup 3 --no-cpu > gpurun_out/misc_c4bdf.json 2> gpurun_out/misc_c4bdf.err
-timeout 900 python bench.py --config c5 --method bdf --trajectories 148 --steps 1 --warmup 3 --no-cpu > gpurun_out/misc_c5bdf.json 2> gpurun_out/misc_c5bdf.err
+timeout 900 python -m pytest tests/test_gpu_timedep.py tests/test_gpu_bdf.py -q -x -p no:cacheprovider > gpurun_out/misc_tests.log 2>&1; echo "rc=$?" >> gpurun_out/misc_tests.log
+timeout 900 python bench.py --config c4td --no-cpu > gpurun_out/misc_c4td.json 2> gpurun_out/misc_c4td.err
