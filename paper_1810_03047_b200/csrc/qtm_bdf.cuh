@@ -19,7 +19,8 @@
 //     kernel (ode.py:261-329, 441-466; trajectory.py:133-250)
 //
 // Mapping.  One CTA per trajectory at a time (persistent, atomic work
-// counter), NT threads own components i = tid + NT*k.  Every vector of the
+// counter; 32 threads for d <= 64, else 256), NT threads own components
+// i = tid + NT*k.  Every vector of the
 // trajectory -- 7 Nordsieck rows, their saved copy, the Newton vectors --
 // and the LU of M live in one per-CTA workspace: dynamic shared memory when
 // it fits (d <= ~100), otherwise a per-CTA slice of HBM (L2-resident for

@@ -686,7 +686,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         // BDF: one kernel per block size; the per-trajectory workspace (history,
         // Newton vectors, LU of the iteration matrix) goes to shared memory when
         // it fits, else to a per-CTA slice of HBM
-        p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
+        // 32 threads for small d (c2 BDF: 2x faster than 128); from d = 65 the
+        // d^2-parallel factorisation / inversion phases want more warps
+        // (c3 BDF: 256 threads +5 % over 128)
+        p->bdf_threads = d->dim <= 64 ? 32 : 256;
         // Newton solves: substitution with the LU (zgetrs) for small d, where
         // the matrix is refactored every few attempts; the explicit inverse
         // (zgetri) for 48 <= d <= 256, where 2d barrier-separated substitution
