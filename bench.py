@@ -439,6 +439,11 @@ def main(argv=None):
                          "peak_source": "measured DFMA throughput on this GPU "
                                         "(qtm_measure_fp64_peak, 2 flops/DFMA)",
                          "flops_per_launch": flops, "kernel_ms": k_ms,
+                         "frac_of_unfused_ceiling": 2.0 * achieved / peak,
+                         "unfused_note": "the arithmetic is deliberately unfused (-fmad=false, "
+                                         "the reference's numba kernels are not fast-math): "
+                                         "every flop is one DMUL/DADD instruction, so half "
+                                         "the DFMA figure is this code's FP64 ceiling",
                          "hbm_equiv_gbs": hbm_equiv,
                          "hbm_equiv_frac": hbm_equiv / hbm_peak if hbm_peak else None,
                          "hbm_peak_gbs": hbm_peak,
