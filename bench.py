@@ -364,6 +364,7 @@ def main(argv=None):
     k_ms = float(np.mean(kernel_ms))
     flops = flops_model(st, packed)
     peak = native.fp64_peak_tflops(local)
+    dmma_peak = native.dmma_peak_tflops(local)
     achieved = flops / (k_ms * 1e-3) / 1e12
     hbm_equiv = bytes_model(st, packed) / (k_ms * 1e-3) / 1e9
     hbm_peak = None
@@ -440,6 +441,9 @@ def main(argv=None):
                                         "(qtm_measure_fp64_peak, 2 flops/DFMA)",
                          "flops_per_launch": flops, "kernel_ms": k_ms,
                          "frac_of_unfused_ceiling": 2.0 * achieved / peak,
+                         "dmma_peak_tflops": dmma_peak,
+                         "dmma_note": "measured FP64 tensor-core (mma.sync m8n8k4 DMMA) "
+                                      "throughput: the ceiling of a dense H_eff path",
                          "unfused_note": "the arithmetic is deliberately unfused (-fmad=false, "
                                          "the reference's numba kernels are not fast-math): "
                                          "every flop is one DMUL/DADD instruction, so half "

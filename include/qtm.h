@@ -183,6 +183,9 @@ int qtm_device_count(void);
 /* measured FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA):
  * the denominator of the FP64 roofline fraction bench.py reports */
 int qtm_measure_fp64_peak(int device, double* tflops);
+/* measured FP64 tensor-core (DMMA m8n8k4) throughput of `device` in TFLOP/s:
+ * the ceiling a dense H_eff path on the FP64 tensor pipe would have */
+int qtm_measure_dmma_peak(int device, double* tflops);
 /* per-phase clock64() totals of thread 0 of every CTA for the last qtm_run
  * (profiling builds compiled with -DQTM_PHASES; zeros otherwise) */
 int qtm_phase_cycles(uint64_t* out16);

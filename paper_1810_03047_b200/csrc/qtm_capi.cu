@@ -1044,4 +1044,55 @@ int qtm_measure_fp64_peak(int device, double* tflops) {
 }
 int qtm_run_resident(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o) { return run_impl(p, a, o, false); }
 
+// FP64 tensor-core probe: independent chains of warp-level DMMA m8n8k4
+// (mma.sync f64; tcgen05 has no FP64 kind on sm_100a).  512 flops per
+// instruction per warp.  Measures whether a dense H_eff path on the FP64
+// tensor pipe could outrun the DFMA pipe.
+__global__ void fp64_dmma_peak_kernel(double* out, int iters) {
+    const double a = threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+    double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c0[j]), "+d"(c1[j])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+    for (int j = 0; j < 4; ++j) s += c0[j] + c1[j];
+    if (s == 1234.5) out[threadIdx.x] = s;
+}
+
+int qtm_measure_dmma_peak(int device, double* tflops) {
+    if (!tflops) return set_error(QTM_ERR_ARGS, "null output");
+    CUDA_TRY(cudaSetDevice(device));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* out = nullptr;
+    CUDA_TRY(cudaMalloc(&out, 1024 * sizeof(double)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 1 << 13, threads = 256, blocks = sms * 8;
+    fp64_dmma_peak_kernel<<<blocks, threads>>>(out, 64);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        fp64_dmma_peak_kernel<<<blocks, threads>>>(out, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (err != cudaSuccess) return set_error(QTM_ERR_CUDA, cudaGetErrorString(err));
+    const double flops = 512.0 * 4.0 * (double)iters * (threads / 32) * blocks;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return QTM_OK;
+}
+
 }  // extern "C"

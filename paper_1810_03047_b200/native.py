@@ -82,7 +82,7 @@ EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_des
            "qtm_max_resident", "qtm_problem_layout",
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
            "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles",
-           "qtm_variant_time_dependent")
+           "qtm_variant_time_dependent", "qtm_measure_dmma_peak")
 
 _lib = None
 
@@ -130,6 +130,8 @@ def lib():
         L.qtm_phase_cycles.restype = C.c_int
     L.qtm_measure_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.qtm_measure_fp64_peak.restype = C.c_int
+    L.qtm_measure_dmma_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    L.qtm_measure_dmma_peak.restype = C.c_int
     if L.qtm_abi_version() != ABI_VERSION:
         raise NativeLibraryError("libqtm.so ABI version mismatch; rebuild it")
     _lib = L
@@ -148,6 +150,14 @@ def variants():
         L.qtm_variant_info(i, C.byref(t), C.byref(e), C.byref(r))
         out.append((t.value, e.value, r.value))
     return out
+
+
+def dmma_peak_tflops(device: int = 0) -> float:
+    out = C.c_double()
+    rc = lib().qtm_measure_dmma_peak(device, C.byref(out))
+    if rc != 0:
+        raise RuntimeError(f"qtm_measure_dmma_peak failed: {last_error()}")
+    return out.value
 
 
 def variant_time_dependent(i: int) -> bool:

@@ -87,3 +87,14 @@ def test_dimension_3000(oracle_lib):
                        options=RunOptions(log_jumps=True))
     pk = pack_problem(p)
     _check(pk, 8, oracle_lib)
+
+
+def test_fp64_pipe_probes():
+    """The roofline denominators are measured on the device: DFMA and the
+    FP64 tensor pipe (DMMA m8n8k4).  B200's FP64 tensor throughput is no
+    higher than its DFMA throughput (why no dense DMMA path)."""
+    from paper_1810_03047_b200 import native
+    dfma = native.fp64_peak_tflops(0)
+    dmma = native.dmma_peak_tflops(0)
+    assert 10.0 < dfma < 100.0 and 5.0 < dmma < 200.0
+    print(f"DFMA {dfma:.1f} TFLOP/s, DMMA {dmma:.1f} TFLOP/s")
