@@ -120,6 +120,11 @@ typedef struct {
     double script_fallback;
     int64_t max_jumps;              /* jump-log capacity per trajectory (0 = no log) */
     void* cuda_stream;              /* cudaStream_t or NULL for the handle's stream */
+    /* psi snapshots: the (unnormalised, interpolated) state each trajectory
+     * records at these grid indices -- the argument the reference passes to
+     * record_expectation (trajectory.py:206-214) -- into qtm_run_out.psi */
+    int32_t n_psi_points;           /* 0 = none */
+    const int64_t* psi_points;      /* [n_psi_points] distinct grid indices */
 } qtm_run_args;
 
 typedef struct {
@@ -152,6 +157,7 @@ typedef struct {
     int32_t grid;         /* CTAs launched */
     int64_t launches;     /* kernels launched by this call */
     int64_t n_failed;     /* trajectories that failed (excluded from the sums) */
+    double* psi;          /* [count][n_psi_points][2*dim] interleaved (or NULL) */
 } qtm_run_out;
 
 int qtm_problem_create(const qtm_problem_desc* desc, qtm_problem** out);

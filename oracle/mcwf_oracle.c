@@ -311,6 +311,9 @@ typedef struct {
     double* w2;
     int has_lu, jac_stale;
     double hl0_fact;
+    /* psi snapshots: slot per grid index (-1 = none) and this trajectory's output */
+    const int32_t* psi_slot;
+    cplx* psi_out;
     /* stats */
     int64_t* st;
 } solver_t;
@@ -664,6 +667,8 @@ static int solver_step(solver_t* S) {
 /* ------------------------------------------------------------- trajectory */
 static int record(solver_t* S, const cplx* psi, int64_t gi, double* values) {
     const mo_problem* P = S->P;
+    if (S->psi_slot && S->psi_slot[gi] >= 0)  /* the state record_expectation receives */
+        memcpy(S->psi_out + (int64_t)S->psi_slot[gi] * S->n, psi, sizeof(cplx) * S->n);
     for (int k = 0; k < P->n_expect; ++k) {
         cplx num;
         double nrm;
@@ -792,6 +797,7 @@ typedef struct {
     const mo_problem* P;
     const mo_run_args* A;
     mo_run_out* O;
+    const int32_t* psi_slot;
     int64_t next;
     int64_t first_fail;
     pthread_mutex_t mu;
@@ -827,6 +833,8 @@ static void* worker(void* arg) {
         int64_t* st = O->stats + row * MO_NSTATS;
         memset(st, 0, sizeof(int64_t) * MO_NSTATS);
         S.st = st;
+        S.psi_slot = sh->psi_slot;
+        S.psi_out = sh->psi_slot ? (cplx*)O->psi + row * (int64_t)A->n_psi_points * n : NULL;
         double* vals = O->values + row * (int64_t)P->n_expect * n_pts;
         int64_t nj = 0;
         mo_error err;
@@ -862,6 +870,14 @@ int mo_run(const mo_problem* P, const mo_run_args* A, mo_run_out* O) {
     if (P->n_td < 0 || (P->n_td > 0 && (P->method != MO_METHOD_ADAMS || !P->td || !P->td_coef))) return MO_ERR_ARGS;
     shared_t sh;
     sh.P = P; sh.A = A; sh.O = O; sh.next = 0; sh.first_fail = -1;
+    int32_t* slot = NULL;
+    if (A->n_psi_points > 0 && A->psi_points && O->psi) {
+        slot = (int32_t*)malloc(sizeof(int32_t) * (P->n_steps + 1));
+        for (int64_t g = 0; g <= P->n_steps; ++g) slot[g] = -1;
+        for (int32_t k = 0; k < A->n_psi_points; ++k)
+            if (A->psi_points[k] >= 0 && A->psi_points[k] <= P->n_steps) slot[A->psi_points[k]] = k;
+    }
+    sh.psi_slot = slot;
     pthread_mutex_init(&sh.mu, NULL);
     memset(&O->error, 0, sizeof(O->error));
     int nt = A->n_threads > 0 ? A->n_threads : 1;
@@ -873,6 +889,7 @@ int mo_run(const mo_problem* P, const mo_run_args* A, mo_run_out* O) {
         free(th);
     }
     pthread_mutex_destroy(&sh.mu);
+    free(slot);
     return sh.first_fail >= 0 ? O->error.code : 0;
 }
 

@@ -80,6 +80,8 @@ typedef struct {
     double script_fallback;
     int64_t max_jumps;            /* jump-log capacity per trajectory */
     int32_t n_threads;
+    int32_t n_psi_points;         /* psi snapshots at these grid indices (0 = none) */
+    const int64_t* psi_points;
 } mo_run_args;
 
 typedef struct {
@@ -98,6 +100,7 @@ typedef struct {
     double* jump_t;      /* [count][max_jumps] or NULL */
     int32_t* jump_idx;   /* [count][max_jumps] or NULL */
     mo_error error;      /* first failing trajectory (lowest index) */
+    double* psi;         /* [count][n_psi_points][2*dim] or NULL */
 } mo_run_out;
 
 int mo_run(const mo_problem* P, const mo_run_args* A, mo_run_out* O);

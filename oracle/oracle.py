@@ -45,7 +45,8 @@ class MoRunArgs(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("traj_begin", C.c_int64), ("traj_end", C.c_int64),
                 ("stream_kind", C.c_int32), ("script", _F64P), ("script_len", _I64P),
                 ("script_stride", C.c_int64), ("script_fallback", C.c_double),
-                ("max_jumps", C.c_int64), ("n_threads", C.c_int32)]
+                ("max_jumps", C.c_int64), ("n_threads", C.c_int32),
+                ("n_psi_points", C.c_int32), ("psi_points", _I64P)]
 
 
 class MoError(C.Structure):
@@ -57,7 +58,7 @@ class MoError(C.Structure):
 class MoRunOut(C.Structure):
     _fields_ = [("values", _F64P), ("stats", _I64P), ("status", C.POINTER(C.c_int32)),
                 ("jump_count", _I64P), ("jump_t", _F64P), ("jump_idx", C.POINTER(C.c_int32)),
-                ("error", MoError)]
+                ("error", MoError), ("psi", _F64P)]
 
 
 _lib = None
@@ -96,12 +97,14 @@ def _csr(m, keep):
 
 def run(packed, seed: int, traj_begin: int, traj_end: int, *, stream: str = "philox",
         n_threads: int | None = None, script=None, script_fallback: float = 0.999999,
-        max_jumps: int = 256):
+        max_jumps: int = 256, psi_points=None):
     """Run trajectories [traj_begin, traj_end) of a PackedProblem on the CPU.
 
     Returns a dict with ``values`` [n, n_expect, n_pts], ``stats`` [n, 16],
-    ``status`` [n], ``jump_count`` [n], ``jump_t``/``jump_idx`` [n, max_jumps]
-    and ``error`` (first failing trajectory, or None)."""
+    ``status`` [n], ``jump_count`` [n], ``jump_t``/``jump_idx`` [n, max_jumps],
+    ``psi`` [n, len(psi_points), dim] (complex, the state recorded at those
+    grid indices; None without psi_points) and ``error`` (first failing
+    trajectory, or None)."""
     L = lib()
     keep = []
     coll = (MoCsr * max(1, packed.n_collapse))(*[_csr(c, keep) for c in packed.collapse])
@@ -127,11 +130,14 @@ def run(packed, seed: int, traj_begin: int, traj_end: int, *, stream: str = "phi
         for i, r in enumerate(rows):
             script_arr[i, : len(r)] = r
             script_len[i] = len(r)
+    pts = None if psi_points is None else np.ascontiguousarray(psi_points, dtype=np.int64)
     args = MoRunArgs(seed & 0xFFFFFFFFFFFFFFFF, traj_begin, traj_end, STREAM_KINDS[stream],
                      _p(script_arr) if script_arr is not None else None,
                      _p(script_len, _I64P) if script_len is not None else None, stride,
                      script_fallback, max_jumps,
-                     n_threads if n_threads else (os.cpu_count() or 1))
+                     n_threads if n_threads else (os.cpu_count() or 1),
+                     0 if pts is None else len(pts), None if pts is None else _p(pts, _I64P))
+    psi = None if pts is None else np.zeros((n, len(pts), packed.dim), dtype=np.complex128)
     values = np.zeros((n, packed.n_expect, packed.n_pts))
     stats = np.zeros((n, NSTATS), np.int64)
     status = np.zeros(n, np.int32)
@@ -140,6 +146,7 @@ def run(packed, seed: int, traj_begin: int, traj_end: int, *, stream: str = "phi
     jidx = np.zeros((n, max_jumps), np.int32)
     out = MoRunOut(_p(values), _p(stats, _I64P), _p(status, C.POINTER(C.c_int32)),
                    _p(jcount, _I64P), _p(jt), _p(jidx, C.POINTER(C.c_int32)))
+    out.psi = psi.view(np.float64).ctypes.data_as(_F64P) if psi is not None else None
     rc = L.mo_run(C.byref(prob), C.byref(args), C.byref(out))
     err = None
     if rc:
@@ -147,7 +154,7 @@ def run(packed, seed: int, traj_begin: int, traj_end: int, *, stream: str = "phi
         err = {"code": e.code, "traj": e.traj, "t": e.t, "h": e.h, "max_steps": e.max_steps,
                "aux": (e.aux0, e.aux1, e.aux2)}
     return {"values": values, "stats": stats, "status": status, "jump_count": jcount,
-            "jump_t": jt, "jump_idx": jidx, "error": err, "rc": rc}
+            "jump_t": jt, "jump_idx": jidx, "error": err, "rc": rc, "psi": psi}
 
 
 def philox_u01(seed: int, k: int, n: int) -> float:

@@ -61,7 +61,8 @@ class QtmRunArgs(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("traj_begin", C.c_int64), ("traj_end", C.c_int64),
                 ("stream_kind", C.c_int32), ("script", _F64P), ("script_len", _I64P),
                 ("script_stride", C.c_int64), ("script_fallback", C.c_double),
-                ("max_jumps", C.c_int64), ("cuda_stream", C.c_void_p)]
+                ("max_jumps", C.c_int64), ("cuda_stream", C.c_void_p),
+                ("n_psi_points", C.c_int32), ("psi_points", _I64P)]
 
 
 class QtmError(C.Structure):
@@ -75,7 +76,8 @@ class QtmRunOut(C.Structure):
                 ("stats_total", _I64P), ("status", _I32P), ("jump_count", _I64P),
                 ("jump_t", _F64P), ("jump_idx", _I32P), ("error", QtmError),
                 ("kernel_ms", C.c_float), ("total_ms", C.c_float), ("variant", C.c_int32),
-                ("grid", C.c_int32), ("launches", C.c_int64), ("n_failed", C.c_int64)]
+                ("grid", C.c_int32), ("launches", C.c_int64), ("n_failed", C.c_int64),
+                ("psi", _F64P)]
 
 
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",

@@ -23,8 +23,12 @@ def _check(name, kind, oracle_lib):
     pk = pack_problem(g.problem)
     k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
     assert np.array_equal(s.traj, np.arange(k0, k1))
-    r = oracle_lib.run(pk, goldens.SEED, k0, k1, stream=kind, script=goldens.SCRIPTS.get(name))
+    r = oracle_lib.run(pk, goldens.SEED, k0, k1, stream=kind, script=goldens.SCRIPTS.get(name),
+                       psi_points=s.psi_points)
     assert r["rc"] == 0, r["error"]
+    # psi(t_j) itself -- the state the reference hands to record_expectation
+    if len(s.psi_points):
+        np.testing.assert_allclose(r["psi"], s.psi, rtol=0, atol=TOL)
     np.testing.assert_array_equal(r["jump_count"], s.jump_count)
     for i in range(len(s.traj)):
         n = s.jump_count[i]
