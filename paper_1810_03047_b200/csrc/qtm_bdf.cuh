@@ -664,6 +664,10 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
         // per-warp partial sums of <psi|E_k|psi> and <psi|psi> (PS complete)
         auto record = [&](int g) {
             __syncthreads();
+            if (R.psi_slot && R.psi_slot[g] >= 0) {
+                double2* const po = R.psi_out + ((size_t)row * R.n_psi + R.psi_slot[g]) * d;
+                for (int i = tid; i < d; i += NT) po[i] = PS[i];
+            }
             double* const rp = R.rec_partial + ((size_t)row * npts + g) * (size_t)(P.ne + 1) * NW + (tid >> 5);
             for (int k = 0; k <= P.ne; ++k) {
                 double acc[1] = {0.0};

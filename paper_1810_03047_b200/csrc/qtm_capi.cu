@@ -225,7 +225,8 @@ struct qtm_problem {
     // run scratch (grown on demand, reused across calls)
     DevBuf<double> values, rec_partial, err, err_r, psum, psq, sum, sumsq, jump_t, script;
     DevBuf<long long> stats, jump_count, script_len, stats_tot;
-    DevBuf<int> status, jump_idx;
+    DevBuf<int> status, jump_idx, psi_slot;
+    DevBuf<double2> psi_out;
     DevBuf<double2> zovf;
     DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row, [2..17] phases
     // BDF method (qtm_bdf.cuh): kernel, block size, workspace placement
@@ -536,6 +537,7 @@ void free_problem(qtm_problem* p) {
     p->sum.release(s); p->sumsq.release(s); p->jump_t.release(s); p->script.release(s);
     p->stats.release(s); p->jump_count.release(s); p->script_len.release(s); p->stats_tot.release(s);
     p->status.release(s); p->jump_idx.release(s); p->zovf.release(s); p->ctl.release(s);
+    p->psi_slot.release(s); p->psi_out.release(s);
     p->bdf_ws.release(s);
     if (s) cudaStreamSynchronize(s);
     for (auto& e : p->ev) if (e) cudaEventDestroy(e);
@@ -770,6 +772,11 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     if (a->stream_kind < 0 || a->stream_kind > 2) return set_error(QTM_ERR_ARGS, "unknown stream kind");
     if (a->stream_kind == QTM_STREAM_SCRIPTED && (!a->script || !a->script_len))
         return set_error(QTM_ERR_ARGS, "scripted stream needs script and script_len");
+    if (a->n_psi_points < 0 || (a->n_psi_points > 0 && !a->psi_points))
+        return set_error(QTM_ERR_ARGS, "psi_points missing");
+    for (int k = 0; k < a->n_psi_points; ++k)
+        if (a->psi_points[k] < 0 || a->psi_points[k] > (int64_t)(p->n_pts - 1))
+            return set_error(QTM_ERR_ARGS, "psi_points index outside the grid");
     std::lock_guard<std::mutex> lock(p->mu);
     CUDA_TRY(cudaSetDevice(p->device));
     const long long count = a->traj_end - a->traj_begin;
@@ -831,6 +838,15 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     CUDA_TRY(p->psq.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));
     CUDA_TRY(p->sumsq.ensure(std::max(n_out, 1), s));
+    const bool want_psi = a->n_psi_points > 0 && o->psi;
+    if (want_psi) {
+        std::vector<int> slot(p->n_pts, -1);
+        for (int k = 0; k < a->n_psi_points; ++k) slot[a->psi_points[k]] = k;
+        CUDA_TRY(p->psi_slot.ensure(p->n_pts, s));
+        CUDA_TRY(cudaMemcpyAsync(p->psi_slot.p, slot.data(), sizeof(int) * p->n_pts, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(p->psi_out.ensure((size_t)run_chunk * a->n_psi_points * p->dim, s));
+        CUDA_TRY(cudaStreamSynchronize(s));  // the host slot table goes out of scope
+    }
     if (a->stream_kind == QTM_STREAM_SCRIPTED) {
         CUDA_TRY(p->script.ensure((size_t)count * std::max<int64_t>(a->script_stride, 1), s));
         CUDA_TRY(p->script_len.ensure(count, s));
@@ -890,6 +906,9 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         R.counter = p->ctl.p;
         R.first_fail = p->ctl.p + 1;
         R.phase_cycles = p->ctl.p + 2;
+        R.psi_slot = want_psi ? p->psi_slot.p : nullptr;
+        R.psi_out = want_psi ? p->psi_out.p : nullptr;
+        R.n_psi = want_psi ? a->n_psi_points : 0;
         BdfParams BP{};
         BP.ws = p->bdf_ws.p;
         BP.ws_stride = p->bdf_ws_elems;
@@ -936,6 +955,9 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
                 CUDA_TRY(cudaMemcpyAsync(o->jump_idx + off * max_jumps, p->jump_idx.p,
                                          sizeof(int32_t) * cnt * max_jumps, cudaMemcpyDeviceToHost, s));
         }
+        if (want_psi)
+            CUDA_TRY(cudaMemcpyAsync(o->psi + off * a->n_psi_points * 2 * p->dim, p->psi_out.p,
+                                     sizeof(double2) * cnt * a->n_psi_points * p->dim, cudaMemcpyDeviceToHost, s));
         if (last) {
             if (n_out > 0) {
                 ensemble_final<<<(n_out + 127) / 128, 128, 0, s>>>(p->psum.p, p->psq.p, (int)n_red_total, n_out,

@@ -153,6 +153,11 @@ struct RunParams {
     unsigned long long* counter;
     unsigned long long* first_fail;  // atomicMin over failing rows
     unsigned long long* phase_cycles;  // [16] (QTM_PHASES builds only)
+    // psi snapshots (diagnostics / parity): slot of each grid index (-1 =
+    // none; nullptr = no snapshots) and the output [n_traj][n_psi][d]
+    const int* psi_slot;
+    double2* psi_out;
+    int n_psi;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -987,6 +992,13 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         // gathered for the ws.row products).
 #define RECORD(psi, gi_)                                                     \
     do {                                                                     \
+        if (R.psi_slot) {                                                    \
+            const int sl__ = R.psi_slot[(gi_)];                              \
+            if (sl__ >= 0) {                                                 \
+                double2* const po__ = R.psi_out + ((size_t)ws.row * R.n_psi + sl__) * d; \
+                _Pragma("unroll") for (int e = 0; e < E; ++e) if (ACT(e)) po__[II(e)] = (psi)[e]; \
+            }                                                                \
+        }                                                                    \
         const double2* xs__ = gath;                                          \
         if (P.e_need_gather) {                                               \
             GATHER(psi, xg__);                                               \

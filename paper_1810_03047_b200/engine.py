@@ -135,6 +135,7 @@ class RunOutput:
     launches: int
     count: int
     n_failed: int = 0
+    psi: np.ndarray | None = None  # [count, n_psi_points, dim] complex, psi_points only
 
 
 def _p(a, t=C.POINTER(C.c_double)):
@@ -208,10 +209,13 @@ class DeviceProblem:
     def run(self, seed: int, traj_begin: int, traj_end: int, *, stream: str = "philox",
             script=None, script_fallback: float = 0.999999, max_jumps: int = 0,
             per_trajectory: bool = True, resident: bool = False,
-            cuda_stream: int | None = None) -> RunOutput:
+            cuda_stream: int | None = None, psi_points=None) -> RunOutput:
         """Integrate global trajectories [traj_begin, traj_end).  With
         ``per_trajectory`` the per-trajectory series, counters and jump logs
-        come back too; ``resident`` skips those copies entirely."""
+        come back too; ``resident`` skips those copies entirely.
+        ``psi_points`` (grid indices) returns each trajectory's state at
+        those points -- the interpolated, unnormalised psi the reference
+        passes to record_expectation (trajectory.py:206-214)."""
         if self._handle is None:
             raise RuntimeError("device problem already closed")
         pk = self.packed
@@ -229,10 +233,13 @@ class DeviceProblem:
             for i, r in enumerate(rows):
                 script_arr[i, : len(r)] = r
                 script_len[i] = len(r)
+        pts = None if psi_points is None else np.ascontiguousarray(psi_points, dtype=np.int64)
         args = native.QtmRunArgs(int(seed) & 0xFFFFFFFFFFFFFFFF, traj_begin, traj_end,
                                  native.STREAM_KINDS[stream], _p(script_arr),
                                  _p(script_len, C.POINTER(C.c_int64)), stride, script_fallback,
-                                 max_jumps, cuda_stream)
+                                 max_jumps, cuda_stream, 0 if pts is None else len(pts),
+                                 _p(pts, C.POINTER(C.c_int64)))
+        psi = None if pts is None else np.zeros((n, len(pts), pk.dim), dtype=np.complex128)
         s = np.zeros(max(n_out, 1))
         s2 = np.zeros(max(n_out, 1))
         tot = np.zeros(native.NSTATS, np.int64)
@@ -247,6 +254,8 @@ class DeviceProblem:
                                _p(tot, C.POINTER(C.c_int64)), _p(status, C.POINTER(C.c_int32)),
                                _p(jc, C.POINTER(C.c_int64)), _p(jt),
                                _p(ji, C.POINTER(C.c_int32)))
+        if psi is not None:
+            out.psi = psi.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))
         L = native.lib()
         with self._lock:
             fn = L.qtm_run_resident if resident else L.qtm_run
@@ -261,7 +270,7 @@ class DeviceProblem:
         return RunOutput(s[:n_out].reshape(pk.n_expect, pk.n_pts),
                          s2[:n_out].reshape(pk.n_expect, pk.n_pts), vals, stats, tot, status, jc,
                          jt, ji, err, rc, out.kernel_ms, out.total_ms, out.variant, out.grid,
-                         out.launches, n, int(out.n_failed))
+                         out.launches, n, int(out.n_failed), psi)
 
 
 _TUNED: dict = {}

@@ -42,7 +42,7 @@ def test_device_matches_reference_goldens(name, kind, oracle_lib):
     s = g.samples[kind]
     k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
     with DeviceProblem(g.problem) as dp:
-        out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ)
+        out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ, psi_points=s.psi_points)
     assert out.rc == 0, out.error
     assert np.all(out.status == 0)
     _, sens_t, sens_v, sens_m = _self_sensitivity(oracle_lib, pack_problem(g.problem), k1 - k0,
@@ -52,6 +52,10 @@ def test_device_matches_reference_goldens(name, kind, oracle_lib):
         assert max(tol_t, tol_v, tol_m) <= 2e-6
     for i in range(k1 - k0):
         _compare(out, s, i, i, tol_t, tol_v)
+    # psi(t_j) itself (north_star: "psi(t) within 1e-6"), the state the
+    # reference handed to record_expectation at these grid points
+    if len(s.psi_points):
+        np.testing.assert_allclose(out.psi, s.psi, rtol=0, atol=tol_v)
     # ensemble over the sample, identical streams
     np.testing.assert_allclose(out.sum / (k1 - k0), s.values.mean(axis=0), rtol=0, atol=tol_m)
     np.testing.assert_array_equal(out.stats[:, native.STAT_NAMES.index("draws")], s.n_draws)
@@ -64,10 +68,12 @@ def test_device_matches_reference_scenarios(name):
         k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
         with DeviceProblem(g.problem) as dp:
             out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ,
-                         script=goldens.SCRIPTS.get(name))
+                         script=goldens.SCRIPTS.get(name), psi_points=s.psi_points)
         assert out.rc == 0, out.error
         for i in range(k1 - k0):
             _compare(out, s, i, i)
+        if len(s.psi_points):
+            np.testing.assert_allclose(out.psi, s.psi, rtol=0, atol=TOL)
 
 
 def _self_sensitivity(oracle_lib, pk, n, stream="philox", begin=0):

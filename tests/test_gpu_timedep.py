@@ -34,11 +34,13 @@ def test_td_device_matches_reference_goldens(name):
     for kind, s in g.samples.items():
         k0, k1 = int(s.traj[0]), int(s.traj[-1]) + 1
         with DeviceProblem(g.problem) as dp:
-            out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ)
+            out = dp.run(goldens.SEED, k0, k1, stream=kind, max_jumps=MAXJ, psi_points=s.psi_points)
         assert out.rc == 0, out.error
         assert native.variant_time_dependent(out.variant)
         _compare(out, s.values, s.jump_count, s.jump_t, s.jump_idx)
         np.testing.assert_array_equal(out.stats[:, 11], s.n_draws)
+        if len(s.psi_points):  # psi(t_j) within 1e-6 of the reference's recorded states
+            np.testing.assert_allclose(out.psi, s.psi, rtol=0, atol=TOL)
 
 
 @pytest.mark.parametrize("name,n", [("td_rabi", 500), ("td_cavity", 256), ("td_ising", 64)])
