@@ -264,20 +264,27 @@ def test_full_size_properties_c4():
     assert np.all(np.abs(mean - mean[::-1]) <= 4 * np.sqrt(se ** 2 + se[::-1] ** 2) + 1e-12)
 
 
-def test_independent_streams_within_three_sigma(oracle_lib):
-    # GPU ensemble at full N (c2) vs an independent-seed CPU ensemble
-    p = configs.build("c2")
+@pytest.mark.parametrize("name,n_cpu", [("c1", 4000), ("c2", 1000), ("c3", 1000), ("c4", 256)])
+def test_independent_streams_within_three_sigma(name, n_cpu, oracle_lib):
+    """GPU ensemble at the config's full N (seed 987654321) vs an
+    independent-seed CPU ensemble: per point
+    |delta| <= 3 sqrt(SE_gpu^2 + SE_cpu^2) up to the expected tail."""
+    p = configs.build(name)
     pk = pack_problem(p)
-    n_gpu, n_cpu = 5000, 1000
+    n_gpu = configs.N_TRAJECTORIES[name]
     with DeviceProblem(pk) as dp:
         out = dp.run(987654321, 0, n_gpu, per_trajectory=False, resident=True)
+    n_ok = n_gpu - out.n_failed  # c4: the reference controller's own two collapses
     ref = oracle_lib.run(pk, 12345, 0, n_cpu)
-    mg = out.sum / n_gpu
-    se_g = np.sqrt(np.maximum(out.sumsq / n_gpu - mg ** 2, 0) / n_gpu)
-    mc = ref["values"].mean(axis=0)
-    se_c = ref["values"].std(axis=0, ddof=1) / np.sqrt(n_cpu)
-    z = np.abs(mg - mc) / np.maximum(np.sqrt(se_g ** 2 + se_c ** 2), 1e-12)
-    # 602 points: allow the expected ~0.3 % beyond 3 sigma, none beyond 5
+    ok = ref["status"] == 0
+    mg = out.sum / n_ok
+    se_g = np.sqrt(np.maximum(out.sumsq / n_ok - mg ** 2, 0) / n_ok)
+    mc = ref["values"][ok].mean(axis=0)
+    se_c = ref["values"][ok].std(axis=0, ddof=1) / np.sqrt(ok.sum())
+    se = np.sqrt(se_g ** 2 + se_c ** 2)
+    live = se > 1e-9  # points where either ensemble has spread (not the shared t = 0 state)
+    z = np.abs(mg - mc)[live] / se[live]
+    # allow the expected ~0.3 % beyond 3 sigma (plus finite-sample slack), none beyond 5
     assert np.mean(z > 3) < 0.02 and z.max() < 5
 
 
