@@ -320,7 +320,7 @@ def main(argv=None):
     if args.method == "bdf":
         args.variant = -1  # one BDF kernel per block size (qtm_bdf.cuh)
     if args.variant == -2:  # untimed: choose the kernel variant on a sample
-        args.variant = autotune_variant(packed, device=local)
+        args.variant = autotune_variant(packed, device=local, n_total=end - begin)
     dp = DeviceProblem(packed, device=local, variant=args.variant)
     for _ in range(args.warmup):
         flush.zero_()  # also loads the fill kernel's module before timing (lazy loading)

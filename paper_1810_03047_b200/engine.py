@@ -290,13 +290,16 @@ def candidate_variants(dim: int, time_dependent: bool = False) -> list[int]:
 
 
 def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | None = None,
-                     seed: int = 987654321) -> int:
+                     seed: int = 987654321, n_total: int | None = None) -> int:
     """Pick the fastest kernel variant for this problem by timing each
-    candidate on a sample of trajectories (result cached per problem digest
-    and device).  The register budget for the Nordsieck history is the main
-    trade-off: enough rows for the orders the problem actually reaches, but
-    no more than needed to keep more warps resident."""
-    key = (packed.digest, device)
+    candidate on a sample of trajectories (result cached per problem digest,
+    device and run size).  The register budget for the Nordsieck history is
+    the main trade-off: enough rows for the orders the problem actually
+    reaches, but no more than needed to keep more warps resident.  With
+    ``n_total`` the sample never exceeds the run: a run that fits in one
+    wave is latency-bound (c1: 500 trajectories), where the variant with the
+    shortest per-trajectory chain wins rather than the one with most CTAs."""
+    key = (packed.digest, device, n_total)
     if key in _TUNED:
         return _TUNED[key]
     cands = candidate_variants(packed.dim, packed.n_td > 0)
@@ -307,7 +310,7 @@ def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | No
         with DeviceProblem(packed, device=device, variant=v) as dp:
             # enough trajectories for several waves of this variant's
             # persistent grid, so the comparison is not decided by the tail
-            n = sample or min(max(6 * dp.max_resident(), 1024), 8192)
+            n = sample or min(max(6 * dp.max_resident(), 1024), 8192, n_total or 8192)
             return min(dp.run(seed, 0, n, resident=True).kernel_ms for _ in range(reps)) / n
 
     # one pass over every candidate, then the three fastest again (best of
