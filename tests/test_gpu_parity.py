@@ -106,7 +106,8 @@ def _self_sensitivity_uncached(oracle_lib, pk, n, stream, begin):
 # the others are the variants bench.py's autotune picks for c4 (256x4, 8
 # register rows), c5 (192x5, 4 register rows, two CTAs per SM; 256x4 was
 # the previous pick), c3 (96x1, 9 rows) and c2 (32x1, history in smem)
-@pytest.mark.parametrize("name,n,variant", [("c1", 500, -1), ("c2", 512, -1), ("c2", 512, 17),
+@pytest.mark.parametrize("name,n,variant", [("c1", 500, -1), ("c1", 500, 0), ("c2", 512, -1),
+                                            ("c2", 512, 17),
                                             ("c3", 256, -1), ("c3", 256, 12),
                                             ("c4", 256, -1), ("c4", 256, 22),
                                             ("c5", 256, -1), ("c5", 256, 15), ("c5", 256, 27)])
