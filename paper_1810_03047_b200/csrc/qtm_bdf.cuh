@@ -161,7 +161,7 @@ constexpr int LU_TILE_ELEMS = LU_NB * LU_MB + LU_NB * 32;
 // and the interchanges commute with the row-wise updates, so the result is
 // bit-identical to the unblocked sweep.  Requires NT = 256.
 template <int NT>
-__device__ void lu_blocked(double2* __restrict__ A, int* __restrict__ ipiv, int d, double2* tiles,
+__device__ __forceinline__ void lu_blocked(double2* __restrict__ A, int* __restrict__ ipiv, int d, double2* tiles,
                            double* s_pv, int* s_pi) {
     static_assert(NT == 256, "tile mapping assumes 8 warps");
     constexpr int NW = NT / 32;
@@ -264,7 +264,7 @@ __device__ void lu_blocked(double2* __restrict__ A, int* __restrict__ ipiv, int 
 }
 
 template <int NT>
-__device__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
+__device__ __forceinline__ void bdf_factor(const DevProblem& P, double2* __restrict__ A, int* __restrict__ ipiv,
                            int* __restrict__ rowat, int* __restrict__ pos, int* __restrict__ dflag,
                            double2* __restrict__ dk, double hl0, double* s_pv, int* s_pi,
                            double2* tiles) {
@@ -405,7 +405,7 @@ __device__ __forceinline__ void block_rows_update(const double2* __restrict__ A,
 // is bit-identical; the L/U columns stream through once, coalesced, with 3
 // barriers per block instead of one per pivot.  b arrives interchanged.
 template <int NT>
-__device__ void bdf_solve_blocked(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
+__device__ __forceinline__ void bdf_solve_blocked(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
                                   const double2* __restrict__ dk, double2* __restrict__ b,
                                   double2* __restrict__ x, double2* tiles) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -473,7 +473,7 @@ __device__ void bdf_solve_blocked(int d, const double2* __restrict__ A, const in
 // The Newton solve then is one parallel matrix-vector product instead of
 // 2d barrier-separated substitution steps.  t: d-vector scratch.
 template <int NT>
-__device__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict__ ipiv,
+__device__ __forceinline__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict__ ipiv,
                            double2* __restrict__ t) {
     const int tid = threadIdx.x;
     for (int j = 0; j < d; ++j) {
@@ -532,7 +532,7 @@ __device__ void bdf_invert(int d, double2* __restrict__ A, const int* __restrict
 
 // x = M^{-1} b with the explicit inverse: row i summed over j in order
 template <int NT>
-__device__ void bdf_apply_inverse(int d, const double2* __restrict__ A, const double2* __restrict__ b,
+__device__ __forceinline__ void bdf_apply_inverse(int d, const double2* __restrict__ A, const double2* __restrict__ b,
                                   double2* __restrict__ x) {
     const int tid = threadIdx.x;
     __syncthreads();
@@ -552,7 +552,7 @@ __device__ void bdf_apply_inverse(int d, const double2* __restrict__ A, const do
 // x = M^{-1} b (zgetrs).  b arrives already interchanged (the caller writes
 // row i of the residual at pos[i]) and is overwritten by the forward sweep.
 template <int NT>
-__device__ void bdf_solve(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
+__device__ __forceinline__ void bdf_solve(int d, const double2* __restrict__ A, const int* __restrict__ dflag,
                           const double2* __restrict__ dk, double2* __restrict__ b,
                           double2* __restrict__ x) {
     const int tid = threadIdx.x;
@@ -599,8 +599,12 @@ __device__ __forceinline__ double2 bdf_horner(const double2* Z, int d, int q, do
     return acc;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT)
+// SMEM: the workspace is the dynamic shared memory (known at compile time,
+// so every workspace access compiles to LDS/STS instead of generic
+// loads/stores that resolve the address space at run time)
+// (one-warp CTAs: capped at 128 registers so ~16 trajectories share an SM)
+template <int NT, bool SMEM>
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1)
 bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R,
            const __grid_constant__ BdfParams B) {
     constexpr int NW = NT / 32;
@@ -615,7 +619,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
     const int tid = threadIdx.x, lane = tid & 31;
     const int d = P.d, npts = P.n_pts;
     const BdfLayout L = BdfLayout::make(d);
-    double2* const ws = B.in_smem ? smem : B.ws + (long long)blockIdx.x * B.ws_stride;
+    double2* const ws = SMEM ? smem : B.ws + (long long)blockIdx.x * B.ws_stride;
     double2* const Z = ws + L.z;
     double2* const SV = ws + L.save;
     double2* const YP = ws + L.ypred;
@@ -751,7 +755,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                     if (!(has_lu && !jac_stale && fabs(hl0 / hl0_fact - 1.0) <= 0.3)) {
                         jac_stale = false;
                         bdf_factor<NT>(P, A, IPIV, ROWAT, POS, DFLAG, DK, hl0, s_pv, s_pi,
-                                       B.in_smem ? nullptr : smem);
+                                       SMEM ? nullptr : smem);
                         if (B.inverse) bdf_invert<NT>(d, A, IPIV, X);
                         st[sLuFactor]++;
                         has_lu = true;
@@ -771,7 +775,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
                         st[sNfe]++;
                         if (B.inverse)
                             bdf_apply_inverse<NT>(d, A, DY, X);
-                        else if (NT == 256 && !B.in_smem)
+                        else if (NT == 256 && !SMEM)
                             bdf_solve_blocked<NT>(d, A, DFLAG, DK, DY, X, smem);
                         else
                             bdf_solve<NT>(d, A, DFLAG, DK, DY, X);

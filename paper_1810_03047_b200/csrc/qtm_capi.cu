@@ -701,10 +701,13 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         if (const char* ev = getenv("QTM_BDF_SOLVE")) p->bdf_inverse = strcmp(ev, "lu") != 0;
         if (const char* ev = getenv("QTM_BDF_THREADS")) {  // A/B experiments
             const int v = atoi(ev);
-            if (v == 32 || v == 128 || v == 256) p->bdf_threads = v;
+            if (v == 32 || v == 256) p->bdf_threads = v;
         }
-        p->bdf_fn = p->bdf_threads == 32 ? (const void*)bdf_kernel<32>
-                    : p->bdf_threads == 128 ? (const void*)bdf_kernel<128> : (const void*)bdf_kernel<256>;
+        const void* const fn_g = p->bdf_threads == 32 ? (const void*)bdf_kernel<32, false>
+                                                      : (const void*)bdf_kernel<256, false>;
+        const void* const fn_s = p->bdf_threads == 32 ? (const void*)bdf_kernel<32, true>
+                                                      : (const void*)bdf_kernel<256, true>;
+        p->bdf_fn = fn_g;  // the static shared memory is the same in both
         p->bdf_ws_elems = BdfLayout::make(d->dim).total;
         cudaFuncAttributes battr;
         size_t bstatic = 4096;
@@ -712,6 +715,7 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         const size_t bcap = (size_t)smem_cap > bstatic ? (size_t)smem_cap - bstatic : 0;
         const size_t bytes = sizeof(double2) * (size_t)p->bdf_ws_elems;
         p->bdf_in_smem = bytes <= bcap;
+        if (p->bdf_in_smem) p->bdf_fn = fn_s;
         // HBM workspace with 256 threads: the blocked LU's tiles in shared memory
         p->smem = p->bdf_in_smem ? bytes : (p->bdf_threads == 256 ? sizeof(double2) * LU_TILE_ELEMS : 0);
         if (cudaFuncSetAttribute(p->bdf_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bcap) != cudaSuccess)
