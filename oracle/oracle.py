@@ -19,7 +19,9 @@ LIB_PATH = os.path.join(HERE, "libmcwf_oracle.so")
 
 NSTATS = 16
 STAT_NAMES = ("attempts", "steps", "corr_fail", "err_reject", "nfe", "corr_iters", "jumps",
-              "bisect", "sum_q", "order_up", "order_down", "draws", "", "", "lu_factor")
+              "bisect", "sum_q", "order_up", "order_down", "draws",
+              "sum_qq1", "overflow_attempts",  # device-only counters (always 0 here)
+              "lu_factor")
 STREAM_KINDS = {"philox": 0, "lfsr113": 1, "scripted": 2}
 
 _I64P = C.POINTER(C.c_int64)
