@@ -30,6 +30,8 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <math_constants.h>
+
 #include "qtm_rng.cuh"
 
 namespace qtm {
@@ -816,6 +818,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     // the register file leaves the registers to the Nordsieck history.
     struct WarpCold {
         double t_lo, r_thr, crate;
+        double t_next;  // P.times[gi] (+inf once every grid point is recorded)
         long long row, steps_in_segment, njumps;
         int gi, nef, ncf;
         unsigned c_att, c_q, c_qq, c_it, c_steps;
@@ -1081,6 +1084,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             DRAW(ws.r_thr);
             COLD_START(P.t_from, psi, P.h0_first);
             ws.gi = 1;
+            ws.t_next = npts > 1 ? P.times[1] : CUDART_INF;
             ws.steps_in_segment = 0;
 
             while (ws.gi < npts) {
@@ -1323,11 +1327,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         if (!found) ts = 0.5 * (a + b);
                     }
                     if (ts <= P.t_to) {
-                        while (ws.gi < npts && P.times[ws.gi] <= ts) {
+                        while (ws.t_next <= ts) {
                             double2 pg[E];
-                            HORNER((P.times[ws.gi] - t) / h, pg);
+                            HORNER((ws.t_next - t) / h, pg);
                             RECORD(pg, ws.gi);
                             ws.gi++;
+                            ws.t_next = ws.gi < npts ? P.times[ws.gi] : CUDART_INF;
                         }
                         // psi(t*) and the collapse (trajectory.py:235-241, 133-154)
                         double2 pst[E];
@@ -1375,11 +1380,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     }
                 }
                 PH_MARK(9);  // [9] jump test (+ jumps)
-                while (ws.gi < npts && P.times[ws.gi] <= t) {
+                while (ws.t_next <= t) {
                     double2 pg[E];
-                    HORNER((P.times[ws.gi] - t) / h, pg);
+                    HORNER((ws.t_next - t) / h, pg);
                     RECORD(pg, ws.gi);
                     ws.gi++;
+                    ws.t_next = ws.gi < npts ? P.times[ws.gi] : CUDART_INF;
                 }
                 PH_MARK(10);  // [10] grid recording
             }
