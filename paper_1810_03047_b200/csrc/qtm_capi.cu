@@ -89,17 +89,22 @@ __global__ void ensemble_final(const double* __restrict__ psum, const double* __
     sumsq[o] = s2;
 }
 
+// per-counter totals over the trajectories: one CTA per counter (slot
+// NSTATS = number of failed trajectories); integer sums, so any order is exact
 __global__ void stats_total(const long long* __restrict__ stats, const int* __restrict__ status,
                             long long n_traj, long long* __restrict__ total) {
-    const int s = threadIdx.x;
-    if (s > NSTATS) return;
+    __shared__ long long part[256];
+    const int s = blockIdx.x;
     long long acc = 0;
-    if (s == NSTATS) {  // slot NSTATS: number of failed trajectories
-        for (long long k = 0; k < n_traj; ++k) acc += status[k] != 0;
-    } else {
-        for (long long k = 0; k < n_traj; ++k) acc += stats[k * NSTATS + s];
+    for (long long k = threadIdx.x; k < n_traj; k += blockDim.x)
+        acc += s == NSTATS ? (long long)(status[k] != 0) : stats[k * NSTATS + s];
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+        __syncthreads();
     }
-    total[s] = acc;
+    if (threadIdx.x == 0) total[s] = part[0];
 }
 
 }  // namespace qtm
@@ -933,7 +938,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
             ensemble_partial<<<g1, 128, 0, s>>>(p->values.p, p->status.p, cnt, n_out, kRedChunk,
                                                 p->psum.p + red_off * n_out, p->psq.p + red_off * n_out);
         }
-        stats_total<<<1, 32, 0, s>>>(p->stats.p, p->status.p, cnt, p->stats_tot.p);
+        stats_total<<<NSTATS + 1, 256, 0, s>>>(p->stats.p, p->status.p, cnt, p->stats_tot.p);
         launches += 1 + 1 + (n_out > 0 ? 1 : 0) + 1;
         CUDA_TRY(cudaGetLastError());
         const bool last = off + kRunChunk >= count;
