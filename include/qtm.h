@@ -18,6 +18,12 @@
  *                           the form of per-point sums and sums of squares.
  *   qtm_problem_destroy  <- end of the problem's lifetime.
  *
+ * Both method families of OdeConfig run on the device: ADAMS (the numba
+ * kernel path, _kernels.py:117-192) and BDF (the general engine's modified
+ * Newton with a dense LU, ode.py:334-423).  A time-dependent right side
+ * (QuantumProblem.rhs_fn, trajectory.py:61, 186) is accepted in the form
+ * H(t) = H0 + sum_k c_k(t) H_k through the n_td/td/td_coef fields (ADAMS).
+ *
  * Plain pointers and sizes only.  The caller owns every host buffer; the
  * problem handle owns the device copies.  A call blocks until its device
  * work is finished; calls on different handles/devices may run concurrently
