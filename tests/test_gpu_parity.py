@@ -340,3 +340,27 @@ def test_ensemble_converges_to_lindblad(name, n, method):
     # (+1e-3: before the first jumps of a finite ensemble its sample SE is 0
     # while the Lindblad curve already carries the O(t) jump probability)
     assert np.all(np.abs(mean - z["values"]) <= 4.5 * se + 1e-3)
+
+
+def test_full_size_c5(oracle_lib):
+    """c5 at BASELINE size (100 000 trajectories, run in two launch chunks):
+    vacuum start <n_j>(0) = 0 exactly, non-negative photon numbers, no
+    failures, and the ensemble within the 3-sigma band of an independent-
+    seed CPU sample."""
+    p = configs.build("c5")
+    pk = pack_problem(p)
+    n = configs.N_TRAJECTORIES["c5"]
+    with DeviceProblem(pk) as dp:
+        out = dp.run(987654321, 0, n, per_trajectory=False, resident=True)
+    assert out.rc == 0 and out.n_failed == 0
+    mean = out.sum / n
+    np.testing.assert_array_equal(mean[:, 0], 0.0)
+    assert np.all(mean >= -1e-12)
+    ref = oracle_lib.run(pk, 12345, 0, 64)
+    assert ref["rc"] == 0
+    se_g = np.sqrt(np.maximum(out.sumsq / n - mean ** 2, 0) / n)
+    se_c = ref["values"].std(axis=0, ddof=1) / np.sqrt(64)
+    se = np.sqrt(se_g ** 2 + se_c ** 2)
+    live = se > 1e-9
+    z = np.abs(mean - ref["values"].mean(axis=0))[live] / se[live]
+    assert np.mean(z > 3) < 0.02 and z.max() < 5
