@@ -236,7 +236,7 @@ def run_reference_arm(args, rank, world):
     desc = (f"{sample} trajectories of {args.config} per step (global indices 0..{sample - 1}, "
             f"Philox streams), oracle/mcwf_oracle.c on {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "trajectories/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "config": args.config,
@@ -246,6 +246,32 @@ def run_reference_arm(args, rank, world):
             "e2e": {"value": value, "unit": "trajectories/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(cmd: list, n: int, env: dict | None = None) -> int:
+    """Start ``cmd`` as ``n`` ranks of one job, the way torchrun would (one
+    process per GPU; RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* in the
+    environment, rendezvous on 127.0.0.1) -- bench.py's own launcher for
+    ``--gpus N`` outside torchrun, as the reference farm spawns its own
+    workers (cluster.py:493-507).  Rank 0's stdout is this process's stdout;
+    the other ranks' stdout goes to stderr.  Returns the worst exit code."""
+    base = dict(os.environ if env is None else env)
+    base.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), WORLD_SIZE=str(n),
+                LOCAL_WORLD_SIZE=str(n))
+    base.setdefault("NCCL_DEBUG", "INFO")
+    procs = []
+    for r in range(n):
+        e = dict(base, RANK=str(r), LOCAL_RANK=str(r))
+        procs.append(subprocess.Popen(cmd, env=e, stdout=None if r == 0 else sys.stderr))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
 
 
 def main(argv=None):
@@ -272,6 +298,12 @@ def main(argv=None):
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not under torchrun: start the N ranks ourselves
+        sys.exit(launch_ranks([sys.executable, os.path.abspath(__file__)] +
+                              list(sys.argv[1:] if argv is None else argv), args.gpus))
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
 
     import torch
     import torch.distributed as dist
@@ -319,8 +351,15 @@ def main(argv=None):
     clocks.start()
     if args.method == "bdf":
         args.variant = -1  # one BDF kernel per block size (qtm_bdf.cuh)
-    if args.variant == -2:  # untimed: choose the kernel variant on a sample
-        args.variant = autotune_variant(packed, device=local, n_total=end - begin)
+    if args.variant == -2:  # untimed: choose the kernel variant on a sample (rank 0's
+        # choice everywhere, so every rank runs the same kernel)
+        if rank == 0:
+            args.variant = autotune_variant(packed, device=local, n_total=end - begin)
+        if world > 1:
+            dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+            v = torch.tensor([args.variant], dtype=torch.int64, device=dev)
+            dist.broadcast(v, src=0)
+            args.variant = int(v.item())
     dp = DeviceProblem(packed, device=local, variant=args.variant)
     for _ in range(args.warmup):
         flush.zero_()  # also loads the fill kernel's module before timing (lazy loading)
@@ -386,7 +425,7 @@ def main(argv=None):
     for _ in range(args.steps):
         if world > 1:
             run_sharded(packed, n_total, SEED, rank=rank, world_size=world, device=local,
-                        on_failure="exclude")
+                        on_failure="exclude", variant=args.variant)
         else:
             with DeviceProblem(packed, device=local, variant=args.variant) as dpe:
                 o = dpe.run(SEED, 0, n_total, resident=True)

@@ -42,7 +42,8 @@
 extern "C" {
 #endif
 
-#define QTM_ABI_VERSION 2   /* 2: BDF method, time-dependent terms */
+#define QTM_ABI_VERSION 3   /* 2: BDF method, time-dependent terms; 3: per-block partial sums */
+#define QTM_BLOCK 256     /* trajectories per fixed-order reduction block */
 #define QTM_LROWS 13      /* Nordsieck rows: Adams order <= 12 (ode.py:46) */
 #define QTM_MAX_OPS 32    /* collapse / expectation operators per problem */
 #define QTM_NSTATS 16
@@ -164,6 +165,14 @@ typedef struct {
     int64_t launches;     /* kernels launched by this call */
     int64_t n_failed;     /* trajectories that failed (excluded from the sums) */
     double* psi;          /* [count][n_psi_points][2*dim] interleaved (or NULL) */
+    /* The ensemble sums are reduced in two fixed stages: per block of
+     * QTM_BLOCK consecutive trajectories (in trajectory order), then over the
+     * blocks in block order, sum = ((0 + b_0) + b_1) + ...  These are the
+     * stage-1 block partials (block i = trajectories traj_begin + 256 i ...),
+     * so shards that start on a block boundary can be combined by another
+     * process into exactly the single-run sums (multi-GPU, run_sharded). */
+    double* block_sum;    /* [ceil(count/QTM_BLOCK)][n_expect*(n_steps+1)] (or NULL) */
+    double* block_sumsq;  /* same shape (or NULL) */
 } qtm_run_out;
 
 int qtm_problem_create(const qtm_problem_desc* desc, qtm_problem** out);

@@ -273,6 +273,14 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
             return set_error(QTM_ERR_ARGS, std::string(what) + ": column index out of range");
         ci[j] = (int)m.col_ind[j];
     }
+    // columns strictly increasing within each row (qtm.h; the reference's
+    // to_csr produces them so, linalg.py): the union-pattern staging of the
+    // time-dependent terms walks rows with one cursor per operator
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = m.row_ptr[i] + 1; j < m.row_ptr[i + 1]; ++j)
+            if (m.col_ind[j] <= m.col_ind[j - 1])
+                return set_error(QTM_ERR_ARGS, std::string(what) +
+                                 ": column indices must be strictly increasing within each row");
     int* drp = nullptr;
     int* dci = nullptr;
     double2* dv = nullptr;
@@ -826,7 +834,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     // of the 256-trajectory reduction block, so the fixed-order ensemble sum
     // is the same as for one launch.
     constexpr long long kRunChunk = 1ll << 16;
-    constexpr int kRedChunk = 256;
+    constexpr int kRedChunk = QTM_BLOCK;
     const long long run_chunk = std::min<long long>(count, kRunChunk);
     const int nw = kthreads / 32;
     const int DP = var.threads * var.comps;
@@ -1010,6 +1018,12 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     if (n_out > 0) {
         memcpy(o->sum, h_sum, sizeof(double) * n_out);
         if (o->sumsq) memcpy(o->sumsq, h_sumsq, sizeof(double) * n_out);
+        if (o->block_sum)
+            CUDA_TRY(cudaMemcpy(o->block_sum, p->psum.p, sizeof(double) * n_red_total * n_out,
+                                cudaMemcpyDeviceToHost));
+        if (o->block_sumsq)
+            CUDA_TRY(cudaMemcpy(o->block_sumsq, p->psq.p, sizeof(double) * n_red_total * n_out,
+                                cudaMemcpyDeviceToHost));
     }
     cudaEventElapsedTime(&o->total_ms, p->ev[0], p->ev[3]);
     o->kernel_ms = kernel_ms;

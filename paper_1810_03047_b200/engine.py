@@ -30,11 +30,11 @@ import numpy as np
 
 from . import native
 from .packing import PackedProblem, pack_problem
-from .problem import OdeFailure, TrajectoryResult
+from .problem import OdeFailure, TrajectoryResult, reference_types
 
 __all__ = ["DeviceProblem", "RunOutput", "run_gpu", "run_sharded", "partition_trajectories",
            "raise_for_status", "stats_dict", "flops_model", "autotune_variant",
-           "candidate_variants"]
+           "candidate_variants", "run_logged", "shard_range", "combine_blocks"]
 
 
 def partition_trajectories(n_total: int, n_workers: int) -> list[int]:
@@ -49,30 +49,52 @@ def partition_trajectories(n_total: int, n_workers: int) -> list[int]:
 
 
 def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
-    counts = partition_trajectories(n_total, world)
-    begin = sum(counts[:rank])
-    return begin, begin + counts[rank]
+    """Rank ``rank``'s contiguous share of the global trajectory indices:
+    whole reduction blocks of ``native.BLOCK`` trajectories, the blocks
+    split by the reference's partition rule (cluster.py:369-377, counts
+    differing by at most one block).  Block-aligned shards make the
+    multi-GPU ensemble sums bitwise equal to a single run's (run_sharded)."""
+    n_blocks = -(-n_total // native.BLOCK)
+    counts = partition_trajectories(n_blocks, world) if n_blocks >= world else \
+        [1 if r < n_blocks else 0 for r in range(world)]
+    b0 = sum(counts[:rank])
+    return min(b0 * native.BLOCK, n_total), min((b0 + counts[rank]) * native.BLOCK, n_total)
 
 
-def _inside(istate: int, detail: str) -> OdeFailure:
+def combine_blocks(block_sum: np.ndarray, block_sumsq: np.ndarray):
+    """Stage 2 of the fixed-order ensemble reduction on the host, in the
+    order of the device's ensemble_final (qtm_capi.cu): ((0 + b_0) + b_1) + ..."""
+    s = np.zeros(block_sum.shape[1:])
+    s2 = np.zeros(block_sum.shape[1:])
+    for b in range(block_sum.shape[0]):
+        s = s + block_sum[b]
+        s2 = s2 + block_sumsq[b]
+    return s, s2
+
+
+def _inside(istate: int, detail: str, problem=None) -> OdeFailure:
     # run_single_trajectory re-raises solver failures with this suffix
     # (trajectory.py:247-248)
-    inner = OdeFailure(istate, detail)
-    return OdeFailure(istate, f"{inner} (inside trajectory)")
+    failure = reference_types(problem)[0]
+    inner = failure(istate, detail)
+    return failure(istate, f"{inner} (inside trajectory)")
 
 
-def raise_for_status(code: int, err: dict) -> None:
-    """Raise the reference's exception for a failing trajectory."""
+def raise_for_status(code: int, err: dict, problem=None) -> None:
+    """Raise the reference's exception for a failing trajectory: an
+    ``OdeFailure`` that is also ``mcwf.ode.OdeFailure`` when the caller uses
+    the reference package (problem.reference_types), else ValueError /
+    RuntimeError exactly where the reference raises them."""
     t, h = err.get("t", 0.0), err.get("h", 0.0)
     if code == native.ERR_MAX_STEPS:
         raise _inside(-1, f"max_steps = {err.get('max_steps')} exhausted in trajectory segment "
-                          f"at t = {t:g}")
+                          f"at t = {t:g}", problem)
     if code == native.ERR_REPEATED_ERRTEST:
-        raise _inside(-4, f"repeated error-test failures at t = {t:g}")
+        raise _inside(-4, f"repeated error-test failures at t = {t:g}", problem)
     if code == native.ERR_STEP_COLLAPSE:
-        raise _inside(-5, f"step size collapsed to {h:g} at t = {t:g}")
+        raise _inside(-5, f"step size collapsed to {h:g} at t = {t:g}", problem)
     if code == native.ERR_CORRECTOR:
-        raise _inside(-5, f"corrector failed to converge at t = {t:g}")
+        raise _inside(-5, f"corrector failed to converge at t = {t:g}", problem)
     if code == native.ERR_BRACKET:
         f_lo, f_hi, r = err.get("aux", (0.0, 0.0, 0.0))
         raise RuntimeError(f"jump bracket violated: norm_sq({t:g}) = {f_lo:g}, "
@@ -136,6 +158,8 @@ class RunOutput:
     count: int
     n_failed: int = 0
     psi: np.ndarray | None = None  # [count, n_psi_points, dim] complex, psi_points only
+    block_sum: np.ndarray | None = None    # [n_blocks, n_expect, n_pts] (block_sums=True)
+    block_sumsq: np.ndarray | None = None
 
 
 def _p(a, t=C.POINTER(C.c_double)):
@@ -209,7 +233,8 @@ class DeviceProblem:
     def run(self, seed: int, traj_begin: int, traj_end: int, *, stream: str = "philox",
             script=None, script_fallback: float = 0.999999, max_jumps: int = 0,
             per_trajectory: bool = True, resident: bool = False,
-            cuda_stream: int | None = None, psi_points=None) -> RunOutput:
+            cuda_stream: int | None = None, psi_points=None,
+            block_sums: bool = False) -> RunOutput:
         """Integrate global trajectories [traj_begin, traj_end).  With
         ``per_trajectory`` the per-trajectory series, counters and jump logs
         come back too; ``resident`` skips those copies entirely.
@@ -256,6 +281,14 @@ class DeviceProblem:
                                _p(ji, C.POINTER(C.c_int32)))
         if psi is not None:
             out.psi = psi.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))
+        bs = bs2 = None
+        if block_sums:
+            nb = -(-n // native.BLOCK)
+            bs = np.zeros((nb, pk.n_expect, pk.n_pts))
+            bs2 = np.zeros((nb, pk.n_expect, pk.n_pts))
+            if n_out > 0 and n > 0:
+                out.block_sum = _p(bs)
+                out.block_sumsq = _p(bs2)
         L = native.lib()
         with self._lock:
             fn = L.qtm_run_resident if resident else L.qtm_run
@@ -270,7 +303,7 @@ class DeviceProblem:
         return RunOutput(s[:n_out].reshape(pk.n_expect, pk.n_pts),
                          s2[:n_out].reshape(pk.n_expect, pk.n_pts), vals, stats, tot, status, jc,
                          jt, ji, err, rc, out.kernel_ms, out.total_ms, out.variant, out.grid,
-                         out.launches, n, int(out.n_failed), psi)
+                         out.launches, n, int(out.n_failed), psi, bs, bs2)
 
 
 _TUNED: dict = {}
@@ -321,19 +354,36 @@ def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | No
     return best
 
 
-def _result(pk: PackedProblem, out: RunOutput, n_ok: int, jumps) -> TrajectoryResult:
+def _result(pk: PackedProblem, out: RunOutput, n_ok: int, jumps, problem=None) -> TrajectoryResult:
     stats = stats_dict(out.stats_total)
     stats["failed"] = out.n_failed
-    return TrajectoryResult(pk.times, out.sum / max(n_ok, 1), n_ok, jumps, sumsq=out.sumsq,
+    return reference_types(problem)[1](pk.times, out.sum / max(n_ok, 1), n_ok, jumps, sumsq=out.sumsq,
                             stats=stats)
 
 
 def _jump_list(out: RunOutput):
+    if out.jump_t is None or int(out.jump_count.max(initial=0)) > out.jump_t.shape[1]:
+        raise RuntimeError("jump log truncated: run with a larger max_jumps "
+                           "(run_logged grows it automatically)")
     jumps = []
     for i in range(out.count):
-        for j in range(int(min(out.jump_count[i], out.jump_t.shape[1]))):
+        for j in range(int(out.jump_count[i])):
             jumps.append((float(out.jump_t[i, j]), int(out.jump_idx[i, j])))
     return jumps
+
+
+def run_logged(dp: "DeviceProblem", seed: int, begin: int, end: int, *, max_jumps: int = 1024,
+               **kw) -> RunOutput:
+    """``dp.run`` with a complete jump log, as the reference keeps every jump
+    (trajectory.py:238-239): the device logs the first ``max_jumps`` jumps of
+    each trajectory and counts all of them; if any trajectory jumped more
+    often, the (deterministic) run is repeated with the capacity raised to
+    the largest count."""
+    out = dp.run(seed, begin, end, max_jumps=max(1, max_jumps), per_trajectory=True, **kw)
+    most = int(out.jump_count.max(initial=0))
+    if most > out.jump_t.shape[1]:
+        out = dp.run(seed, begin, end, max_jumps=most, per_trajectory=True, **kw)
+    return out
 
 
 def run_gpu(problem, n_total: int, master_seed: int, *, device: int = 0,
@@ -353,59 +403,96 @@ def run_gpu(problem, n_total: int, master_seed: int, *, device: int = 0,
     with DeviceProblem(problem, device=device, variant=variant) as dp:
         if log_jumps is None:
             log_jumps = dp.packed.log_jumps
-        out = dp.run(master_seed, 0, n_total, stream=stream,
-                     max_jumps=max_jumps if log_jumps else 0, per_trajectory=log_jumps)
+        if log_jumps:
+            out = run_logged(dp, master_seed, 0, n_total, stream=stream, max_jumps=max_jumps)
+        else:
+            out = dp.run(master_seed, 0, n_total, stream=stream, per_trajectory=False)
         if out.rc != 0 and on_failure == "raise":
-            raise_for_status(out.rc, out.error)
+            raise_for_status(out.rc, out.error, problem)
         return _result(dp.packed, out, n_total - out.n_failed,
-                       _jump_list(out) if log_jumps else None)
+                       _jump_list(out) if log_jumps else None, problem)
 
 
 def run_sharded(problem, n_total: int, master_seed: int, *, rank: int, world_size: int,
                 stream: str = "philox", device: int | None = None, runner=None,
-                group=None, on_failure: str = "raise") -> TrajectoryResult | None:
+                group=None, on_failure: str = "raise", variant: int = -1) -> TrajectoryResult | None:
     """One rank of a multi-GPU run (one process per GPU, torch.distributed
-    initialised by the caller).  Rank r integrates its contiguous range of
-    global trajectory indices; the per-point sums, sums of squares, counters
-    and the first failure are combined with one all-reduce.  Returns the
-    TrajectoryResult on every rank.
+    initialised by the caller).  Rank r integrates its contiguous,
+    block-aligned range of global trajectory indices (shard_range); the
+    reduction-block partials, counters, failure count and every rank's first
+    failing trajectory travel in ONE float64 SUM all-reduce:
 
-    ``runner(packed, seed, begin, end, stream) -> RunOutput`` defaults to the
-    device engine on ``device`` (= rank); the CPU multi-process tests inject
-    the oracle here to check the sharding and reduction logic with gloo."""
+        [block_sum | block_sumsq | stats | n_failed | first_fail[world] | setup_error[world]]
+
+    Every slot is written by exactly one rank (the others contribute 0), so
+    the all-reduce is exact, and every rank then adds the blocks in block
+    order like the device's own ensemble_final: the sums are bitwise those of
+    a single-GPU run, whatever the number of ranks.  (first_fail[r] = 1 + the
+    global index of rank r's lowest failing trajectory, 0 if none.)  A rank
+    whose device setup or launch raises still joins the collective with
+    setup_error[r] = 1, so no rank is left waiting, and every rank raises
+    afterwards.  Returns the TrajectoryResult on every rank.
+
+    ``runner(packed, seed, begin, end, stream) -> RunOutput`` (with
+    block_sum / block_sumsq) defaults to the device engine on ``device``
+    (= rank); the CPU multi-process tests inject the oracle here to check
+    the sharding and reduction logic with gloo."""
     import torch
     import torch.distributed as dist
 
     packed = problem if isinstance(problem, PackedProblem) else pack_problem(problem)
     begin, end = shard_range(n_total, world_size, rank)
-    if runner is None:
-        dev = rank if device is None else device
-        with DeviceProblem(packed, device=dev) as dp:
-            out = dp.run(master_seed, begin, end, stream=stream, per_trajectory=False,
-                         resident=True)
-    else:
-        out = runner(packed, master_seed, begin, end, stream)
     n_out = packed.n_expect * packed.n_pts
-    fail_row = out.error["traj"] if out.rc != 0 else np.iinfo(np.int64).max
+    n_blocks = -(-n_total // native.BLOCK)
+    out, local_exc = None, None
+    try:
+        if end <= begin:
+            out = None
+        elif runner is None:
+            dev = rank if device is None else device
+            with DeviceProblem(packed, device=dev, variant=variant) as dp:
+                out = dp.run(master_seed, begin, end, stream=stream, per_trajectory=False,
+                             resident=True, block_sums=True)
+        else:
+            out = runner(packed, master_seed, begin, end, stream)
+    except Exception as exc:  # joined below, re-raised after the collective
+        local_exc = exc
+    tab = 2 * n_blocks * n_out
+    base = tab + native.NSTATS + 1
+    vec = np.zeros(base + 2 * world_size)
+    if local_exc is not None:
+        vec[base + world_size + rank] = 1
+    elif out is not None:
+        b0 = begin // native.BLOCK
+        nb = out.block_sum.shape[0]
+        blocks = vec[:tab].reshape(2, n_blocks, n_out)
+        blocks[0, b0:b0 + nb] = out.block_sum.reshape(nb, n_out)
+        blocks[1, b0:b0 + nb] = out.block_sumsq.reshape(nb, n_out)
+        vec[tab:tab + native.NSTATS] = out.stats_total
+        vec[tab + native.NSTATS] = out.n_failed
+        if out.rc != 0:
+            vec[base + rank] = 1 + int(out.error["traj"])
     backend = dist.get_backend(group)
     tdev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else \
         torch.device("cpu")
-    # one float64 all-reduce: [sum | sumsq | stats | failed]
-    buf = torch.from_numpy(np.concatenate([out.sum.ravel(), out.sumsq.ravel(),
-                                           out.stats_total.astype(np.float64),
-                                           [float(out.n_failed)]])).to(tdev)
+    buf = torch.from_numpy(vec).to(tdev)
     dist.all_reduce(buf, group=group)
-    fail = torch.tensor([fail_row], dtype=torch.int64, device=tdev)
-    dist.all_reduce(fail, op=dist.ReduceOp.MIN, group=group)
-    first_fail = int(fail.item())
-    if first_fail != np.iinfo(np.int64).max and on_failure == "raise":
-        if out.rc != 0 and out.error["traj"] == first_fail:
-            raise_for_status(out.rc, out.error)
-        raise RuntimeError(f"trajectory {first_fail} failed on another rank")
     host = buf.cpu().numpy()
-    s = host[:n_out].reshape(packed.n_expect, packed.n_pts)
-    s2 = host[n_out:2 * n_out].reshape(packed.n_expect, packed.n_pts)
-    stats = stats_dict(host[2 * n_out:2 * n_out + native.NSTATS].astype(np.int64))
-    stats["failed"] = int(host[-1])
+    if local_exc is not None:
+        raise local_exc
+    bad = [r for r in range(world_size) if host[base + world_size + r] != 0]
+    if bad:
+        raise RuntimeError(f"rank(s) {bad} failed before integrating their trajectories")
+    fails = [int(x) - 1 for x in host[base:base + world_size] if x != 0]
+    if fails and on_failure == "raise":
+        first_fail = min(fails)
+        if out is not None and out.rc != 0 and out.error["traj"] == first_fail:
+            raise_for_status(out.rc, out.error, problem)
+        raise RuntimeError(f"trajectory {first_fail} failed on another rank")
+    blocks = host[:tab].reshape(2, n_blocks, packed.n_expect, packed.n_pts)
+    s, s2 = combine_blocks(blocks[0], blocks[1])
+    stats = stats_dict(host[tab:tab + native.NSTATS].astype(np.int64))
+    stats["failed"] = int(host[tab + native.NSTATS])
     n_ok = n_total - stats["failed"]
-    return TrajectoryResult(packed.times, s / max(n_ok, 1), n_ok, None, sumsq=s2, stats=stats)
+    return reference_types(problem)[1](packed.times, s / max(n_ok, 1), n_ok, None, sumsq=s2,
+                                       stats=stats)

@@ -346,10 +346,12 @@ def _drain_until_shutdown(transport) -> None:
 
 def _device_runner(device: int, stream: str, max_jumps: int):
     def run(problem, seed, begin, end, log_jumps):
-        from .engine import DeviceProblem, _jump_list
+        from .engine import DeviceProblem, _jump_list, run_logged
         with DeviceProblem(problem, device=device) as dp:
-            out = dp.run(seed, begin, end, stream=stream,
-                         max_jumps=max_jumps if log_jumps else 0, per_trajectory=log_jumps)
+            if log_jumps:
+                out = run_logged(dp, seed, begin, end, stream=stream, max_jumps=max_jumps)
+            else:
+                out = dp.run(seed, begin, end, stream=stream, per_trajectory=False)
         return out, (_jump_list(out) if log_jumps and out.rc == 0 else None)
     return run
 
@@ -393,7 +395,7 @@ def run_gpu_worker(transport, problem, rank: int, *, device: int = 0, stream: st
         # the lowest failing trajectory, with the reference's message text
         local = int(out.error["traj"]) - base
         try:
-            raise_for_status(out.rc, out.error)
+            raise_for_status(out.rc, out.error, problem)
             text = f"trajectory failed with status {out.rc}"
         except (RuntimeError, ValueError) as exc:
             text = str(exc)

@@ -13,7 +13,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QTM_LIB") or os.path.join(HERE, "libqtm.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
+BLOCK = 256  # QTM_BLOCK: trajectories per fixed-order reduction block
 NSTATS = 16
 LROWS = 13
 MAX_OPS = 32
@@ -77,7 +78,7 @@ class QtmRunOut(C.Structure):
                 ("jump_t", _F64P), ("jump_idx", _I32P), ("error", QtmError),
                 ("kernel_ms", C.c_float), ("total_ms", C.c_float), ("variant", C.c_int32),
                 ("grid", C.c_int32), ("launches", C.c_int64), ("n_failed", C.c_int64),
-                ("psi", _F64P)]
+                ("psi", _F64P), ("block_sum", _F64P), ("block_sumsq", _F64P)]
 
 
 EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_destroy",

@@ -284,3 +284,58 @@ def auto_step(g, y0: np.ndarray, rtol: float, atol: float, f0=None) -> float:
     if fw <= 0.0:
         return 1e-6
     return 0.01 / fw
+
+
+# -- the reference's own result / exception types at the boundary ---------------
+
+_REF_TYPES: dict = {}
+
+
+def _reference_module(problem=None):
+    """The reference package ``mcwf`` when the caller uses it: the problem
+    is an ``mcwf`` object, or ``mcwf`` is already imported.  (Never imported
+    just for this -- the device path does not depend on the reference.)"""
+    import sys
+    mod = type(problem).__module__.split(".")[0] if problem is not None else ""
+    if mod == "mcwf" or "mcwf" in sys.modules:
+        try:
+            import mcwf  # noqa: F401
+            import mcwf.ode
+            import mcwf.trajectory
+            return sys.modules["mcwf"]
+        except ImportError:
+            return None
+    return None
+
+
+def reference_types(problem=None):
+    """``(OdeFailure, TrajectoryResult)`` classes for results handed back to
+    the caller.  With ``mcwf`` in use they are subclasses of BOTH the
+    reference's classes (``mcwf.ode.OdeFailure``, ode.py:53-62, and
+    ``mcwf.trajectory.TrajectoryResult``, trajectory.py:106-119) and this
+    package's mirrors, so ``except mcwf.OdeFailure`` and
+    ``isinstance(r, mcwf.TrajectoryResult)`` hold for device results while
+    ``sumsq`` / ``stats`` / ``standard_error()`` stay available."""
+    mc = _reference_module(problem)
+    if mc is None:
+        return OdeFailure, TrajectoryResult
+    key = id(mc)
+    if key not in _REF_TYPES:
+        from dataclasses import dataclass as _dc
+
+        class DeviceOdeFailure(mc.ode.OdeFailure, OdeFailure):
+            __module__ = __name__
+
+            def __init__(self, istate: int, detail: str):
+                RuntimeError.__init__(
+                    self, f"HALT: Error in ode solver, value ISTATE = {istate} ({detail})")
+                self.istate = istate
+
+        @_dc(frozen=True)
+        class DeviceTrajectoryResult(mc.trajectory.TrajectoryResult, TrajectoryResult):
+            __module__ = __name__
+
+        DeviceOdeFailure.__qualname__ = DeviceOdeFailure.__name__ = "OdeFailure"
+        DeviceTrajectoryResult.__qualname__ = DeviceTrajectoryResult.__name__ = "TrajectoryResult"
+        _REF_TYPES[key] = (DeviceOdeFailure, DeviceTrajectoryResult)
+    return _REF_TYPES[key]

@@ -1,8 +1,9 @@
 """BASELINE configs c1-c5 built with the REFERENCE constructors.
 
-Used only by ``make_golden.py`` in the build container (where
-/root/reference is mounted).  The concrete inputs follow SURVEY.md §8d;
-the GPU box never imports this module.
+Used by ``make_golden.py`` / ``make_scale_golden.py`` in the build
+container (where /root/reference is mounted) and by the drop-in tests
+(tests/test_dropin*.py), which import the reference from baseline/_ref when
+/root/reference is absent.  The concrete inputs follow SURVEY.md §8d.
 """
 
 from __future__ import annotations
@@ -10,7 +11,16 @@ from __future__ import annotations
 import sys
 from math import sqrt
 
-REF_SRC = "/root/reference/pkg/src"
+import os
+
+# the reference package: its source tree in the build container, else the
+# copy pip-installed into baseline/_ref (travels to the GPU box)
+_REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+REF_SRC = next((p for p in ("/root/reference/pkg/src", os.path.join(_REPO, "baseline", "_ref"))
+                if os.path.isdir(os.path.join(p, "mcwf"))), None)
+if REF_SRC is None:
+    raise ImportError("the reference package mcwf is not available (no /root/reference, "
+                      "no baseline/_ref)")
 if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 

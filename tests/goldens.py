@@ -85,3 +85,30 @@ BDF_NAMES = ("bdf_c1", "bdf_c2", "bdf_c3", "bdf_stiff", "bdf_decay_forced_jump")
 SCRIPTS = {"decay_forced_jump": [[0.5, 0.3, 0.9999999]],
            "bdf_decay_forced_jump": [[0.5, 0.3, 0.9999999]],
            "decay_no_jump": [[float(np.exp(-1.0) / 2)]]}
+
+
+@dataclass
+class Scale:
+    """BASELINE-scale reference outputs (tests/golden/scale_<cN>.npz, made by
+    make_scale_golden.py from the reference itself)."""
+    name: str
+    samples: dict          # kind -> Sample (+ .status per trajectory)
+    status: dict           # kind -> [n] ISTATE of an OdeFailure (0 = completed)
+    n_psi: int
+    farm: dict             # the reference's own run_local_farm ensemble
+    raw: dict
+
+
+def load_scale(name: str) -> Scale:
+    z = dict(np.load(os.path.join(GOLDEN_DIR, f"scale_{name}.npz"), allow_pickle=False))
+    samples, status = {}, {}
+    for kind in ("philox", "lfsr113"):
+        counts = z[f"{kind}_jump_count"]
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        jt = [z[f"{kind}_jump_t"][offs[i]:offs[i + 1]] for i in range(len(counts))]
+        ji = [z[f"{kind}_jump_idx"][offs[i]:offs[i + 1]] for i in range(len(counts))]
+        samples[kind] = Sample(kind, z[f"{kind}_traj"], z[f"{kind}_values"], counts, jt, ji,
+                               1 + 2 * counts, z[f"{kind}_psi_points"], z[f"{kind}_psi"])
+        status[kind] = z[f"{kind}_status"]
+    farm = {k[5:]: z[k] for k in z if k.startswith("farm_")}
+    return Scale(name, samples, status, int(z["philox_n_psi"]), farm, z)

@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import goldens
+from sensitivity import self_sensitivity
 from paper_1810_03047_b200 import configs, engine, native
 from paper_1810_03047_b200.engine import DeviceProblem, run_gpu
 from paper_1810_03047_b200.packing import pack_problem
@@ -77,29 +78,7 @@ def test_device_matches_reference_scenarios(name):
 
 
 def _self_sensitivity(oracle_lib, pk, n, stream="philox", begin=0):
-    """How far the reference algorithm's own trajectories move when its
-    first step size is perturbed by one ulp: the floor for any
-    implementation that is not bit-identical to it.  (c5 -- 29k attempts
-    per trajectory over t in [0, 40] -- moves its jump times by ~3e-6.)"""
-    key = (pk.digest, n, stream, begin)
-    if key not in _SENS:
-        _SENS[key] = _self_sensitivity_uncached(oracle_lib, pk, n, stream, begin)
-    return _SENS[key]
-
-
-_SENS: dict = {}
-
-
-def _self_sensitivity_uncached(oracle_lib, pk, n, stream, begin):
-    import dataclasses
-    a = oracle_lib.run(pk, goldens.SEED, begin, begin + n, max_jumps=MAXJ, stream=stream)
-    pk2 = dataclasses.replace(pk, h0_first=float(np.nextafter(pk.h0_first, 1.0)))
-    b = oracle_lib.run(pk2, goldens.SEED, begin, begin + n, max_jumps=MAXJ, stream=stream)
-    dt = max(float(np.abs(a["jump_t"][i, :a["jump_count"][i]]
-                          - b["jump_t"][i, :a["jump_count"][i]]).max(initial=0.0))
-             for i in range(n) if a["jump_count"][i] == b["jump_count"][i])
-    dmean = float(np.abs(a["values"].mean(axis=0) - b["values"].mean(axis=0)).max())
-    return a, dt, float(np.abs(a["values"] - b["values"]).max()), dmean
+    return self_sensitivity(oracle_lib, pk, n, stream, begin)
 
 
 # (config, sample size, kernel variant): -1 = the default for the dimension

@@ -133,7 +133,10 @@ def test_packing_layout():
 
 def test_partition_rule():
     assert engine.partition_trajectories(10, 3) == [4, 3, 3]
-    assert engine.shard_range(10, 3, 1) == (4, 7)
+    # shards are whole 256-trajectory reduction blocks (bitwise rank-count
+    # invariance, engine.shard_range); the blocks follow the same rule
+    assert engine.shard_range(10, 3, 0) == (0, 10) and engine.shard_range(10, 3, 1) == (10, 10)
+    assert engine.shard_range(3000, 3, 1) == (1024, 2048)
     assert sum(engine.partition_trajectories(4096, 8)) == 4096
     with pytest.raises(ValueError):
         engine.partition_trajectories(0, 2)

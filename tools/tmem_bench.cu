@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(NT, 1) tmem_kernel(int iters, int mode, unsign
     __syncthreads();
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-        const uint32_t a = ta + (uint32_t)((it & 7) * 16);
+        const uint32_t a = ta + (uint32_t)((it & (mode == 3 ? 1 : 7)) * 16);
         if (mode == 0) {
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
                          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -36,6 +36,41 @@ __global__ void __launch_bounds__(NT, 1) tmem_kernel(int iters, int mode, unsign
                            "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                          : "r"(a));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc += r[i];
+        } else if (mode == 2) {
+            // read-modify-write of 16 words (4 complex doubles): the Nordsieck
+            // row update pattern (ld, wait, add, st)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                           "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                           "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                         : "r"(a));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] += 3u;
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+                         :: "r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                            "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]),
+                            "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+        } else if (mode == 3) {
+            // 4 independent x16 loads, one wait (the batched row read pattern)
+            uint32_t q[48];
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                             : "=r"(q[16*j+0]), "=r"(q[16*j+1]), "=r"(q[16*j+2]), "=r"(q[16*j+3]), "=r"(q[16*j+4]), "=r"(q[16*j+5]),
+                               "=r"(q[16*j+6]), "=r"(q[16*j+7]), "=r"(q[16*j+8]), "=r"(q[16*j+9]), "=r"(q[16*j+10]), "=r"(q[16*j+11]),
+                               "=r"(q[16*j+12]), "=r"(q[16*j+13]), "=r"(q[16*j+14]), "=r"(q[16*j+15])
+                             : "r"(a + 16u * j));
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                           "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                           "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                         : "r"(a + 48u));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int i = 0; i < 48; ++i) acc += q[i];
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc += r[i];
         } else {
@@ -72,16 +107,16 @@ void run(int mode) {
     double avg = 0;
     for (int i = 0; i < grid; ++i) avg += h[i];
     avg /= grid;
-    const double bytes = (double)iters * NT * 16 * 4;  // per CTA
+    const double bytes = (double)iters * NT * 16 * 4 * (mode == 3 ? 4 : 1);  // per CTA
+    static const char* names[] = {"ld", "st", "rmw", "ld4"};
     printf("%s NT=%d: %s  %.0f cycles, %.1f B/cycle/SM (%.1f cycles per warp-instruction)\n",
-           mode ? "st" : "ld", NT, cudaGetErrorString(e), avg, bytes / avg,
+           names[mode], NT, cudaGetErrorString(e), avg, bytes / avg,
            avg / iters);
     cudaFree(cyc);
     cudaFree(sink);
 }
 
 int main() {
-    run<128>(0); run<256>(0); run<512>(0);
-    run<128>(1); run<256>(1); run<512>(1);
+    for (int m = 0; m < 4; ++m) { run<32>(m); run<128>(m); run<256>(m); run<512>(m); }
     return 0;
 }
