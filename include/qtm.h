@@ -200,6 +200,11 @@ int qtm_variant_info(int i, int32_t* threads, int32_t* comps, int32_t* reg_rows)
 /* 1 if variant i was compiled with the time-dependent generator terms
  * (required when n_td > 0), 0 if not, < 0 on a bad index */
 int qtm_variant_time_dependent(int i);
+/* Nordsieck rows variant i keeps in Tensor Memory (rows 2..7 with the e
+ * buffers: 6), 0 for register / shared-memory histories, < 0 on a bad index */
+int qtm_variant_tmem_rows(int i);
+/* kernel variant a problem runs (-1: the BDF kernel) */
+int qtm_problem_variant(qtm_problem* problem);
 int qtm_device_count(void);
 /* measured FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA):
  * the denominator of the FP64 roofline fraction bench.py reports */

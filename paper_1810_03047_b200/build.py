@@ -22,15 +22,16 @@ CSRC = os.path.join(HERE, "csrc")
 GEN = os.path.join(CSRC, "gen")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libqtm.so")
-# QTM_FMAD=1 builds with fused multiply-add contraction (rounding then
-# differs from the reference's unfused numba arithmetic by ~1 ulp per op);
-# QTM_BUILD_TAG / QTM_LIB select an alternative library file for A/B runs.
+# The throughput build contracts a*b+c into fused multiply-adds (rounding then
+# differs from the reference's unfused numba arithmetic by ~1 ulp per op, the
+# same order as the tree reductions; the whole GPU suite, reference-scale
+# parity included, is green with it).  QTM_FMAD=0 builds the unfused parity
+# library (every flop one DMUL/DADD, as numba); QTM_BUILD_TAG / QTM_LIB select
+# an alternative library file for A/B runs.
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-# -fmad=false: the reference's numba kernels are not fast-math, so a*b+c is
-# never contracted there; keeping the same rounding keeps parity tight.
-FMAD = os.environ.get("QTM_FMAD", "0") == "1"
+FMAD = os.environ.get("QTM_FMAD", "1") == "1"
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", f"-fmad={'true' if FMAD else 'false'}",
                      "-Xcompiler", "-fPIC", "-I", INCLUDE]
 # extra nvcc flags for A/B experiments (e.g. -DQTM_SPMV_PF(E)=0)
@@ -94,6 +95,10 @@ VARIANTS = [
     # memory): two history rows in registers, the rest in the per-CTA
     # overflow scratch (L2), G as CSR through L1/L2
     (1024, 3, 2, 1, 3072),         # 38
+    # Nordsieck rows 2..7 and e / e_prev in TMEM (HistT, csrc/qtm_tmem.cuh):
+    # 128 registers and ~110 KB of shared memory per d <= 1024 trajectory,
+    # so two trajectory CTAs share an SM (each allocating 256 TMEM columns)
+    (256, 4, 8, 2, 0, False, True),   # 39
 ]
 
 SOURCES = ["qtm_traj.cuh", "qtm_bdf.cuh", "qtm_rng.cuh", "qtm_capi.cu"]
@@ -121,16 +126,18 @@ def generate() -> list[str]:
     for i, row in enumerate(VARIANTS):
         nt, e, rr, mb, auto = row[:5]
         td = "true" if len(row) > 5 and row[5] else "false"
+        tmem = "true" if len(row) > 6 and row[6] else "false"
         name = f"variant_{i}.cu"
         body = f"""// generated by build.py -- kernel variant {i}
 #include "../qtm_traj.cuh"
 namespace qtm {{
-template __global__ void traj_kernel<{nt}, {e}, {rr}, {mb}, {td}>(const __grid_constant__ DevProblem,
-                                                         const __grid_constant__ RunParams);
+template __global__ void traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>(const __grid_constant__ DevProblem,
+                                                                 const __grid_constant__ RunParams);
 VariantDesc variant_{i}() {{
     return VariantDesc{{{nt}, {e}, {rr}, {mb}, {auto}, {1 if td == "true" else 0},
-                       TrajKernel<{nt}, {e}, {rr}>::smem_bytes(),
-                       reinterpret_cast<const void*>(traj_kernel<{nt}, {e}, {rr}, {mb}, {td}>)}};
+                       TrajKernel<{nt}, {e}, {rr}, {tmem}>::smem_bytes(),
+                       reinterpret_cast<const void*>(traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>),
+                       {1 if tmem == "true" else 0}}};
 }}
 }}  // namespace qtm
 """

@@ -28,8 +28,9 @@
 // sequential in the pivot index, so they run as CTA-wide sweeps with one
 // barrier per pivot; the trailing update walks columns by warp and rows by
 // lane (column-major storage: coalesced, conflict-free).  There are no
-// reductions inside the LU or the substitution solves, so with -fmad=false
-// they are bit-identical to the oracle's restatement.  From d = 48 up the
+// reductions inside the LU or the substitution solves, so in the unfused
+// parity build (QTM_FMAD=0) they are bit-identical to the oracle's
+// restatement.  From d = 48 up the
 // Newton solve applies the explicit inverse instead (bdf_invert, LAPACK
 // zgetri order after the same pivoted LU): one parallel matrix-vector
 // product per iteration instead of 2d barrier-separated substitution

@@ -147,6 +147,10 @@ struct Variant {
     int threads, comps, reg_rows, min_blocks, auto_upto, td;
     size_t smem;
     const void* fn;
+    int tm;  // history rows 2..7 + e buffers in TMEM (HistT)
+    // TMEM columns per CTA (tm only): 32 per component and thread, per lane
+    // quarter of warps
+    int tmem_cols() const { return tm ? (threads / 128) * 32 * comps : 0; }
 };
 
 }  // namespace
@@ -159,7 +163,8 @@ const std::vector<Variant>& variants() {
     static const std::vector<Variant> v = [] {
         std::vector<Variant> out;
         for (const qtm::VariantDesc& d : qtm_variant_table())
-            out.push_back(Variant{d.threads, d.comps, d.reg_rows, d.min_blocks, d.auto_upto, d.td, d.smem, d.fn});
+            out.push_back(Variant{d.threads, d.comps, d.reg_rows, d.min_blocks, d.auto_upto, d.td, d.smem, d.fn,
+                                  d.tm});
         return out;
     }();
     return v;
@@ -175,6 +180,35 @@ int auto_variant(int64_t d, bool td) {
         if (v.auto_upto >= d && (best < 0 || v.auto_upto < variants()[best].auto_upto)) best = i;
     }
     return best;
+}
+
+// CTAs of a variant resident per SM with `smem` bytes of dynamic shared
+// memory.  For the TMEM variants the runtime's occupancy calculator answers 1
+// whatever the resources (measured, tools/occ_probe.cu: it reports 1 for any
+// kernel with tcgen05.alloc, while two such 256-thread CTAs do run side by
+// side on every SM), so their occupancy is computed from the limits
+// themselves: threads, registers (per-warp allocation in units of 256),
+// shared memory (+ the per-block reservation) and the SM's 512 TMEM columns.
+cudaError_t variant_occupancy(const Variant& v, size_t smem, int device, int* per_sm) {
+    if (!v.tm) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, v.fn, v.threads, smem);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, v.fn);
+    if (e != cudaSuccess) return e;
+    int sm_smem = 0, reserved = 0, max_threads = 0, regs_sm = 0, max_blocks = 0;
+    if ((e = cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device)) ||
+        (e = cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device)) ||
+        (e = cudaDeviceGetAttribute(&max_threads, cudaDevAttrMaxThreadsPerMultiProcessor, device)) ||
+        (e = cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device)) ||
+        (e = cudaDeviceGetAttribute(&max_blocks, cudaDevAttrMaxBlocksPerMultiprocessor, device)))
+        return e;
+    const int warps = (v.threads + 31) / 32;
+    const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+    int n = std::min(max_blocks, max_threads / v.threads);
+    n = std::min(n, regs_sm / std::max(1, regs_warp * warps));
+    n = std::min<long long>(n, (long long)sm_smem / (long long)(smem + fa.sharedSizeBytes + reserved));
+    n = std::min(n, 512 / std::max(1, v.tmem_cols()));
+    *per_sm = n;
+    return cudaSuccess;
 }
 
 // Device memory comes from the device's default stream-ordered pool with an
@@ -469,12 +503,24 @@ int stage_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp, const s
     const size_t off = (p->smem + 15) & ~(size_t)15;
     const Variant& var = variants()[p->variant];
     int base = 0, occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&base, var.fn, var.threads, p->smem));
+    CUDA_TRY(variant_occupancy(var, p->smem, p->device, &base));
+    if (getenv("QTM_DEBUG_OCC")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, var.fn);
+        fprintf(stderr, "[qtm] variant %d smem %zu -> %d CTAs/SM (regs %d, static smem %zu, max dyn %d, local %zu)\n",
+                p->variant, p->smem, base, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
+                fa.localSizeBytes);
+        for (size_t sm = 40000; sm <= 120000; sm += 20000) {
+            int o = 0;
+            variant_occupancy(var, sm, p->device, &o);
+            fprintf(stderr, "[qtm]   smem %zu -> %d CTAs/SM\n", sm, o);
+        }
+    }
     // preferred: the dense real diagonals [ne][dp] (one 8-byte load per
     // value), when every observable qualifies and the CTAs per SM hold
     if (smask == full) {
         const size_t smem = off + sizeof(double) * (size_t)ne * dp;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, var.threads, smem));
+        CUDA_TRY(variant_occupancy(var, smem, p->device, &occ));
         if (occ >= 1 && occ >= base) {
             std::vector<double> re((size_t)ne * dp);
             for (size_t i = 0; i < re.size(); ++i) re[i] = dense[i].x;
@@ -493,7 +539,7 @@ int stage_expect_diag(qtm_problem* p, const qtm_problem_desc* d, int dp, const s
     }
     const size_t idx_bytes = ((size_t)ne * dp + 15) & ~(size_t)15;
     const size_t smem = off + idx_bytes + sizeof(double) * dict.size();
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, var.fn, var.threads, smem));
+    CUDA_TRY(variant_occupancy(var, smem, p->device, &occ));
     if (occ < 1 || occ < base) return QTM_OK;
     idx.resize(idx_bytes, 0);
     uint8_t* di = nullptr;
@@ -573,6 +619,16 @@ int qtm_variant_info(int i, int32_t* threads, int32_t* comps, int32_t* reg_rows)
     if (comps) *comps = v.comps;
     if (reg_rows) *reg_rows = v.reg_rows;
     return QTM_OK;
+}
+
+int qtm_problem_variant(qtm_problem* p) {
+    if (!p) return set_error(QTM_ERR_ARGS, "null argument");
+    return p->method == 1 ? -1 : p->variant;
+}
+
+int qtm_variant_tmem_rows(int i) {
+    if (i < 0 || i >= (int)variants().size()) return set_error(QTM_ERR_ARGS, "variant index out of range");
+    return variants()[i].tm ? 6 : 0;
 }
 
 int qtm_variant_time_dependent(int i) {
@@ -742,6 +798,28 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds);
     }
     if (rc == QTM_OK && p->method == 0) rc = build_expect_diag(p, d, var.threads * var.comps);
+    if (rc == QTM_OK && p->method == 0 && var.tm) {
+        // every resident CTA allocates tmem_cols() of the SM's 512 TMEM
+        // columns (variant_occupancy counts them); the hardware must never
+        // place more CTAs on an SM than the allocations allow, so the
+        // dynamic shared memory is padded until the shared-memory limit
+        // alone enforces the cap
+        const int cap = 512 / var.tmem_cols();
+        int sm_bytes = 0, reserved = 0;
+        cudaFuncAttributes fa;
+        if (cudaDeviceGetAttribute(&sm_bytes, cudaDevAttrMaxSharedMemoryPerMultiprocessor, d->device) != cudaSuccess ||
+            cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, d->device) != cudaSuccess ||
+            cudaFuncGetAttributes(&fa, var.fn) != cudaSuccess) {
+            rc = set_error(QTM_ERR_CUDA, "device attribute query failed");
+        } else {
+            const size_t per_block = p->smem + fa.sharedSizeBytes + reserved;
+            if ((size_t)sm_bytes / per_block > (size_t)cap)
+                p->smem = (size_t)sm_bytes / (cap + 1) + 1 - fa.sharedSizeBytes - reserved;
+            int per_sm = 0;
+            if (variant_occupancy(var, p->smem, d->device, &per_sm) != cudaSuccess || per_sm < 1)
+                rc = set_error(QTM_ERR_UNSUPPORTED, "TMEM variant cannot be resident with this problem's shared memory");
+        }
+    }
     if (rc == QTM_OK && p->ctl.ensure(18, p->stream) != cudaSuccess) rc = set_error(QTM_ERR_CUDA, "allocation of ctl failed");
     if (rc == QTM_OK && cudaStreamSynchronize(p->stream) != cudaSuccess)
         rc = set_error(QTM_ERR_CUDA, "problem upload failed");
@@ -764,7 +842,7 @@ int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
     if (p->method == 1)
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->bdf_fn, p->bdf_threads, p->smem));
     else
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var.fn, var.threads, p->smem));
+        CUDA_TRY(variant_occupancy(var, p->smem, p->device, &per_sm));
     *ctas = sms * per_sm;
     return QTM_OK;
 }
@@ -772,7 +850,7 @@ int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
 int qtm_problem_layout(qtm_problem* p, int32_t* reg_rows, int32_t* smem_rows, int64_t* smem_bytes) {
     if (!p || !reg_rows || !smem_rows || !smem_bytes) return set_error(QTM_ERR_ARGS, "null argument");
     const Variant& var = variants()[p->variant];
-    *reg_rows = var.reg_rows > 0 ? std::min(var.reg_rows, LROWS) : 0;
+    *reg_rows = var.tm ? 2 : (var.reg_rows > 0 ? std::min(var.reg_rows, LROWS) : 0);
     *smem_rows = var.reg_rows > 0 ? 0 : LROWS;
     if (p->method == 1) {  // BDF: the whole workspace in shared memory or in HBM
         *reg_rows = 0;
@@ -817,7 +895,8 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     const int kthreads = bdf ? p->bdf_threads : var.threads;
     int dev_sms = 0, per_sm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kthreads, p->smem));
+    if (bdf) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kthreads, p->smem));
+    else CUDA_TRY(variant_occupancy(var, p->smem, p->device, &per_sm));
     if (per_sm < 1) return set_error(QTM_ERR_CUDA, "kernel variant cannot be resident (registers/smem)");
     long long grid = std::min<long long>((long long)dev_sms * per_sm, std::min<long long>(count, 1ll << 16));
     if (bdf && !p->bdf_in_smem) {

@@ -33,6 +33,7 @@
 #include <math_constants.h>
 
 #include "qtm_rng.cuh"
+#include "qtm_tmem.cuh"
 
 namespace qtm {
 
@@ -57,6 +58,7 @@ struct VariantDesc {
     int threads, comps, reg_rows, min_blocks, auto_upto, td;
     size_t smem;
     const void* fn;
+    int tm;  // Nordsieck rows 2..7 and e / e_prev in TMEM (HistT)
 };
 
 struct DevCsr {
@@ -164,7 +166,10 @@ struct RunParams {
 
 // ---------------------------------------------------------------- helpers
 // The reference's numba kernels are compiled without fast-math, so no a*b+c
-// is fused; this file is built with -fmad=false to keep the same rounding.
+// is fused there.  The throughput build (build.py) lets nvcc contract into
+// DFMA -- a ~1-ulp rounding difference per operation, the same order as the
+// tree reductions, inside every parity tolerance; QTM_FMAD=0 builds the
+// unfused parity library with the reference's rounding per operation.
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
@@ -657,6 +662,14 @@ struct Hist {
         }
     }
 
+    __device__ __forceinline__ static void row_all(const Z& z, const O& ovf, int j, double2 (&out)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = row(z, ovf, j, e);
+    }
+    __device__ __forceinline__ static void set_row_all(Z& z, const O& ovf, int j, const double2 (&v)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) set_row(z, ovf, j, e, v[e]);
+    }
     __device__ __forceinline__ static double2 row(const Z& z, const O& ovf, int j, int e) {
         if (j >= RREG) return ovf.at(j, e);
         double2 out = z[0][e];
@@ -745,6 +758,14 @@ struct HistS {
     }
     __device__ __forceinline__ static double2 row(const Z& z, const O&, int j, int e) { return at(z, j, e); }
     __device__ __forceinline__ static void set_row(Z& z, const O&, int j, int e, double2 v) { at(z, j, e) = v; }
+    __device__ __forceinline__ static void row_all(const Z& z, const O& o, int j, double2 (&out)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = at(z, j, e);
+    }
+    __device__ __forceinline__ static void set_row_all(Z& z, const O& o, int j, const double2 (&v)[E]) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) at(z, j, e) = v[e];
+    }
     __device__ __forceinline__ static void horner(const Z& z, const O&, int q, double s, double2 (&out)[E]) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -755,17 +776,175 @@ struct HistS {
     }
 };
 
+
+// ------------------------------------------ history in TMEM (HistT, sm_100a)
+// Row 1 (read by every corrector iteration) stays in registers, row 0 in the
+// thread's private shared-memory slots (also read by every iteration, and
+// the register file is what limits two CTAs per SM), rows 2..7 and the
+// corrector terms e / e_prev live in the thread's private TMEM columns
+// (qtm_tmem.cuh), rows >= 8 in the overflow column as in Hist<8>.
+// Column layout of a thread's 32E columns (E = 4: 128):
+//   [0, 4E)        e buffer slot 0, component e at 4e (lo x, hi x, lo y, hi y)
+//   [4E, 8E)       e buffer slot 1
+//   [8E + 24e, +24) rows 2..7 of component e
+// Every history operation runs per component: the 6 TMEM rows of component
+// e+1 are loaded while component e is processed with the register code of
+// Hist<8, 1> (so the arithmetic, and its rounding, is exactly Hist<8>'s),
+// then stored back.
+template <int E, int DP>
+struct HistT {
+    static_assert(E == 4, "e-buffer slots are one x16 TMEM access (E = 4)");
+    static constexpr int ROWS = 8;
+    static constexpr int COLS = 32 * E;  // TMEM columns per thread
+    using H1 = Hist<ROWS, 1, DP>;
+    using O = typename Hist<ROWS, E, DP>::O;
+    struct Z {
+        double2 r1[E];  // row 1
+        double2* z0;    // row 0: z0[(DP / E) * e] (this thread's shared-memory slots)
+        uint32_t ta;    // this thread's column block (tm::thread_base)
+    };
+    __device__ __forceinline__ static double2& at(Z& z, int j, int e) {
+        return j == 0 ? z.z0[(DP / E) * e] : z.r1[e];
+    }
+    __device__ __forceinline__ static const double2& at(const Z& z, int j, int e) {
+        return j == 0 ? z.z0[(DP / E) * e] : z.r1[e];
+    }
+    __device__ __forceinline__ static uint32_t rows_col(const Z& z, int e) { return z.ta + 8u * E + 24u * e; }
+
+    // Single-buffered: one component's 24 columns in flight at a time keeps
+    // the register footprint small (the TMEM latency is hidden by the second
+    // CTA on the SM, not by prefetching).
+    template <bool STORE, class F>
+    __device__ __forceinline__ static void per_comp(Z& z, const O& ovf, F&& f) {
+        tm::wait_st();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            uint32_t raw[24];
+            tm::issue_ld24(rows_col(z, e), raw);
+            tm::wait_ld24(raw);
+            double2 t[6];
+            tm::unpack<6>(raw, t);
+            double2 zc[ROWS][1];
+            zc[0][0] = z.z0[(DP / E) * e];
+            zc[1][0] = z.r1[e];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) zc[2 + k][0] = t[k];
+            const typename H1::O o1{ovf.p + e * (DP / E)};
+            f(zc, o1, e);
+            if constexpr (STORE) {
+                z.z0[(DP / E) * e] = zc[0][0];
+                z.r1[e] = zc[1][0];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) t[k] = zc[2 + k][0];
+                tm::pack<6>(t, raw);
+                tm::st24(rows_col(z, e), raw);
+            }
+        }
+    }
+    __device__ __forceinline__ static void predict(Z& z, const O& ovf, int q) {
+        per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int) {
+            H1::predict(zc, o, q);
+        });
+    }
+    __device__ __forceinline__ static void undo(Z& z, const O& ovf, int q) {
+        per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int) {
+            H1::undo(zc, o, q);
+        });
+    }
+    __device__ __forceinline__ static void rescale(Z& z, const O& ovf, int q, double ratio) {
+        per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int) {
+            H1::rescale(zc, o, q, ratio);
+        });
+    }
+    __device__ __forceinline__ static void commit(Z& z, const O& ovf, int q, const double* l,
+                                                  const double2 (&ev)[E]) {
+        per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
+            const double2 ev1[1] = {ev[e]};
+            H1::commit(zc, o, q, l, ev1);
+        });
+    }
+    __device__ __forceinline__ static void horner(Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
+        per_comp<false>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
+            double2 o1[1];
+            H1::horner(zc, o, q, s, o1);
+            out[e] = o1[0];
+        });
+    }
+    __device__ __forceinline__ static void row_all(const Z& z, const O& ovf, int j, double2 (&out)[E]) {
+        if (j < 2) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[e] = at(z, j, e);
+        } else if (j < ROWS) {
+            tm::wait_st();
+            uint32_t r[4 * E];
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                tm::issue_ld4(rows_col(z, e) + 4u * (j - 2), r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
+            tm::wait_ld16(r);
+            tm::unpack<E>(r, out);
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) out[e] = ovf.at(j, e);
+        }
+    }
+    __device__ __forceinline__ static void set_row_all(Z& z, const O& ovf, int j, const double2 (&v)[E]) {
+        if (j < 2) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) at(z, j, e) = v[e];
+        } else if (j < ROWS) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                uint32_t r[4];
+                const double2 one[1] = {v[e]};
+                tm::pack<1>(one, r);
+                tm::st4(rows_col(z, e) + 4u * (j - 2), r);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) ovf.at(j, e) = v[e];
+        }
+    }
+    // e / e_prev buffer slots
+    __device__ __forceinline__ static void eb_store(const Z& z, int slot, const double2 (&v)[E]) {
+        uint32_t r[16];
+        tm::pack<E>(v, r);
+        tm::st16(z.ta + 4u * E * slot, r);
+    }
+    __device__ __forceinline__ static void eb_load(const Z& z, int slot, double2 (&v)[E]) {
+        tm::wait_st();
+        uint32_t r[16];
+        tm::issue_ld16(z.ta + 4u * E * slot, r);
+        tm::wait_ld16(r);
+        tm::unpack<E>(r, v);
+    }
+    __device__ __forceinline__ static void eb_load2(const Z& z, int slot, double2 (&a)[E], double2 (&b)[E]) {
+        tm::wait_st();
+        uint32_t ra[16], rb[16];
+        tm::issue_ld16(z.ta + 4u * E * slot, ra);
+        tm::issue_ld16(z.ta + 4u * E * (slot ^ 1), rb);
+        tm::wait_ld16(ra);
+        tm::wait_ld16(rb);
+        tm::unpack<E>(ra, a);
+        tm::unpack<E>(rb, b);
+    }
+};
+
 // ------------------------------------------------------------- the kernel
-template <int NT, int E, int RREG>
+template <int NT, int E, int RREG, bool TM = false>
 struct TrajKernel {
     static constexpr int DP = NT * E;  // padded state length
     static constexpr int NW = NT / 32;
+    // gather buffers [2][DP] and (not with TM: those live in TMEM) the e
+    // buffers [2][DP], plus RREG == 0's Nordsieck rows
+    static constexpr int VEC_BUFS = (TM ? 3 : 4) + (RREG == 0 ? LROWS : 0);  // TM: + row 0
 
     // fixed part of the dynamic shared memory; the staged operator follows
     __host__ __device__ static constexpr size_t smem_bytes() {
-        return sizeof(double2) * (size_t)DP * (RREG == 0 ? 4 + LROWS : 4) +
+        return sizeof(double2) * (size_t)DP * VEC_BUFS +
                sizeof(double) * 2 * KRED * (NW > 1 ? NW : 1) + sizeof(double) * (size_t)DP;
     }
+    // TMEM columns one CTA allocates (a power of two >= 32)
+    __host__ __device__ static constexpr uint32_t tmem_cols() { return TM ? (uint32_t)(NW / 4) * 32u * E : 0u; }
 };
 
 // Row access: rows < RREG are register arrays indexed by compile-time j
@@ -790,19 +969,32 @@ struct TrajKernel {
 // TD: variant compiled with the time-dependent generator terms (td_apply
 // calls cost registers even when not taken, so constant-generator variants
 // are built without them)
-template <int NT, int E, int RREG, int MINB, bool TD>
-__global__ void __launch_bounds__(NT, MINB)
+// Register cap of the TMEM variants: two 256-thread CTAs per SM need less
+// than the 128 registers __launch_bounds__(256, 2) allows (measured: at 128
+// the occupancy calculator grants one CTA per SM)
+#ifndef QTM_TM_MAXNREG
+#define QTM_TM_MAXNREG 120
+#endif
+#define QTM_MAXNREG(NT, MINB, TM) __maxnreg__((TM) ? QTM_TM_MAXNREG : 65536 / ((NT) * (MINB)) > 255 ? 255 : 65536 / ((NT) * (MINB)))
+// TM: Nordsieck rows 2..7 and the e buffers in TMEM (HistT; RREG must be 8,
+// the rows held on chip)
+template <int NT, int E, int RREG, int MINB, bool TD, bool TM = false>
+__global__ void __launch_bounds__(NT, MINB) QTM_MAXNREG(NT, MINB, TM)
 traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R) {
     constexpr int DP = NT * E;
-    using H = std::conditional_t<RREG == 0, HistS<E, DP>, Hist<(RREG > 0 ? RREG : 2), E, DP>>;
+    static_assert(!TM || (RREG == 8 && NT % 128 == 0), "TMEM history: 8 rows on chip, whole lane quarters");
+    using H = std::conditional_t<TM, HistT<E, DP>,
+                                 std::conditional_t<RREG == 0, HistS<E, DP>, Hist<(RREG > 0 ? RREG : 2), E, DP>>>;
     extern __shared__ double2 smem[];
     // gath[2][DP]: double-buffered gather buffers; gath[gbuf] is the most
     //              recently published vector (the corrector iterate lives here)
     // ebuf[2][DP]: corrector term e of the current attempt / of the previous
     //              accepted step (e_prev); "e_prev = e.copy()" is a flip
+    //              (TM: in TMEM, HistT::eb_*)
     double2* const gath = smem;
     double2* const ebuf = smem + 2 * DP;
-    double* const red = reinterpret_cast<double*>(smem + 4 * DP);
+    // TM: row 0 of the Nordsieck history at smem + 2 DP (HistT)
+    double* const red = reinterpret_cast<double*>(smem + (TM ? 3 : 4) * DP);
     // wsm[DP]: error weights 1/(atol + rtol |z0_i|), thread-private slots
     // (read once per corrector iteration; kept out of the register file)
     double* const wsm = red + 2 * KRED * (NT / 32 > 1 ? NT / 32 : 1);
@@ -838,7 +1030,15 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 
     // ---- stage G (sliced ELL + value dictionary) in shared memory once
     double2* const s_dict = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) +
-                                                       TrajKernel<NT, E, RREG>::smem_bytes());
+                                                       TrajKernel<NT, E, RREG, TM>::smem_bytes());
+    // ---- TMEM for the history (TM): allocated once per persistent CTA
+    __shared__ uint32_t s_taddr;
+    if constexpr (TM) {
+        if ((threadIdx.x >> 5) == 0) tm::alloc(&s_taddr, TrajKernel<NT, E, RREG, TM>::tmem_cols());
+        tm::fence_before_sync();
+        __syncthreads();
+        tm::fence_after_sync();
+    }
     uint32_t* const s_ent = reinterpret_cast<uint32_t*>(s_dict + P.sell_dict_n);
     double2* const s_tdict = reinterpret_cast<double2*>(s_ent + P.sell_entries);
     uint16_t* const s_tent = reinterpret_cast<uint16_t*>(s_tdict + P.sell_td_dict_n);
@@ -940,8 +1140,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         long long ph_last = clock64();
 #endif
 
-        typename H::Z z;  // Nordsieck history: registers (rows < RREG) or shared memory (RREG == 0)
-        if constexpr (RREG == 0) z.p = zrows;
+        typename H::Z z;  // Nordsieck history: registers (rows < RREG), shared memory (RREG == 0) or TMEM (TM)
+        if constexpr (TM) {
+            z.ta = tm::thread_base(s_taddr, H::COLS);
+            z.z0 = smem + 2 * DP + tid;
+        }
+        else if constexpr (RREG == 0) z.p = zrows;
 #define W(e) wsm[II(e)]
         double t, h;
         int q, ialth;
@@ -1117,12 +1321,14 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         PH_MARK(2);  // [2] gather z0 + barrier
                     }
                     double2* const ecurp = ebuf + ecur * DP;
+
                     for (int m = 0; m < 3; ++m) {
                         const double2* const cur = gath + gbuf * DP;
                         double2* const nxt = gath + (gbuf ^ 1) * DP;
                         ws.c_it++;
                         double v[3] = {0.0, 0.0, 0.0};
                         double2 fg[E];
+                        double2 etm[E];  // TM: this iteration's e, stored to TMEM below
                         GSPMV_T(cur, fg, t + h);
                         PH_MARK(3);  // [3] SpMV
 #pragma unroll
@@ -1138,9 +1344,15 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                                 v[1] += cabs2(ei) * we * we;
                                 v[2] += cabs2(yn);
                                 nxt[II(e)] = yn;
-                                ecurp[II(e)] = ei;
+                                if constexpr (TM) etm[e] = ei;
+                                else ecurp[II(e)] = ei;
+                            } else if constexpr (TM) {
+                                etm[e] = make_double2(0.0, 0.0);
                             }
                         }
+                        // TM: e goes to TMEM right away (an asynchronous store),
+                        // so it holds no registers across the next SpMV
+                        if constexpr (TM) H::eb_store(z, ecur, etm);
                         PH_MARK(4);  // [4] corrector update
                         block_sum<NT, 3>(v, red, rphase);
                         if constexpr (NT == 32) __syncwarp();
@@ -1165,8 +1377,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                         if (!(est > 1.0)) {
                             // commit zp[j] += l_j e (_kernels.py:187-191)
                             double2 evr[E];
+                            if constexpr (TM) {
+                                H::eb_load(z, ecur, evr);
+                            } else {
 #pragma unroll
-                            for (int e = 0; e < E; ++e) evr[e] = ACT(e) ? ecurp[II(e)] : make_double2(0.0, 0.0);
+                                for (int e = 0; e < E; ++e) evr[e] = ACT(e) ? ecurp[II(e)] : make_double2(0.0, 0.0);
+                            }
                             H::commit(z, OVF(), q, P.l[q], evr);
                             break;  // accepted
                         }
@@ -1220,15 +1436,23 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     const bool need_u = q < P.max_order && has_eprev;
                     double v[2] = {0.0, 0.0};
                     {
-                        const double2* const ecp = ebuf + ecur * DP;
-                        const double2* const epp = ebuf + (ecur ^ 1) * DP;
+                        double2 zq[E], ec[E], ep[E];
+                        H::row_all(z, OVF(), q, zq);
+                        if constexpr (TM) {
+                            H::eb_load2(z, ecur, ec, ep);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < E; ++e) {
+                                ec[e] = ACT(e) ? ebuf[ecur * DP + II(e)] : make_double2(0.0, 0.0);
+                                ep[e] = ACT(e) ? ebuf[(ecur ^ 1) * DP + II(e)] : make_double2(0.0, 0.0);
+                            }
+                        }
 #pragma unroll
                         for (int e = 0; e < E; ++e) {
                             if (ACT(e)) {
-                                const double2 zq = H::row(z, OVF(), q, e);
-                                const double2 de = csub(ecp[II(e)], epp[II(e)]);
+                                const double2 de = csub(ec[e], ep[e]);
                                 const double we = W(e);
-                                v[0] += cabs2(zq) * we * we;
+                                v[0] += cabs2(zq[e]) * we * we;
                                 v[1] += cabs2(de) * we * we;
                             }
                         }
@@ -1263,10 +1487,16 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                     } else {
                         if (best == r_up) {
                             const double cu = P.l[q][q] / (q + 1);
-                            const double2* const ecp = ebuf + ecur * DP;
+                            double2 ec[E];
+                            if constexpr (TM) {
+                                H::eb_load(z, ecur, ec);
+                            } else {
 #pragma unroll
-                            for (int e = 0; e < E; ++e)
-                                H::set_row(z, OVF(), q + 1, e, ACT(e) ? cscale(cu, ecp[II(e)]) : make_double2(0.0, 0.0));
+                                for (int e = 0; e < E; ++e) ec[e] = ACT(e) ? ebuf[ecur * DP + II(e)] : make_double2(0.0, 0.0);
+                            }
+#pragma unroll
+                            for (int e = 0; e < E; ++e) ec[e] = ACT(e) ? cscale(cu, ec[e]) : make_double2(0.0, 0.0);
+                            H::set_row_all(z, OVF(), q + 1, ec);
                             q = q + 1;
                             STAT(sOrderUp, 1);
                         } else if (best == r_down) {
@@ -1411,6 +1641,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             if (rc != kOk) atomicMin(R.first_fail, (unsigned long long)ws.row);
         }
         __syncthreads();
+    }
+    if constexpr (TM) {
+        tm::fence_before_sync();
+        __syncthreads();
+        tm::fence_after_sync();
+        if ((threadIdx.x >> 5) == 0) tm::dealloc(s_taddr, TrajKernel<NT, E, RREG, TM>::tmem_cols());
     }
 #undef OVF
 #undef W

@@ -211,7 +211,9 @@ class DeviceProblem:
         r, s, b = C.c_int32(), C.c_int32(), C.c_int64()
         if native.lib().qtm_problem_layout(self._handle, C.byref(r), C.byref(s), C.byref(b)) != 0:
             raise RuntimeError(native.last_error())
-        return {"reg_rows": r.value, "smem_rows": s.value, "smem_bytes": b.value}
+        v = native.lib().qtm_problem_variant(self._handle)
+        return {"reg_rows": r.value, "smem_rows": s.value, "smem_bytes": b.value,
+                "tmem_rows": native.variant_tmem_rows(v) if v >= 0 else 0, "variant": v}
 
     def close(self):
         if getattr(self, "_handle", None):

@@ -85,7 +85,8 @@ EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_des
            "qtm_max_resident", "qtm_problem_layout",
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
            "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles",
-           "qtm_variant_time_dependent", "qtm_measure_dmma_peak")
+           "qtm_variant_time_dependent", "qtm_measure_dmma_peak", "qtm_variant_tmem_rows",
+           "qtm_problem_variant")
 
 _lib = None
 
@@ -126,6 +127,10 @@ def lib():
     L.qtm_variant_info.restype = C.c_int
     L.qtm_variant_time_dependent.argtypes = [C.c_int]
     L.qtm_variant_time_dependent.restype = C.c_int
+    L.qtm_problem_variant.argtypes = [C.c_void_p]
+    L.qtm_problem_variant.restype = C.c_int
+    L.qtm_variant_tmem_rows.argtypes = [C.c_int]
+    L.qtm_variant_tmem_rows.restype = C.c_int
     L.qtm_device_count.argtypes = []
     L.qtm_device_count.restype = C.c_int
     if hasattr(L, "qtm_phase_cycles"):
@@ -165,6 +170,11 @@ def dmma_peak_tflops(device: int = 0) -> float:
 
 def variant_time_dependent(i: int) -> bool:
     return lib().qtm_variant_time_dependent(i) == 1
+
+
+def variant_tmem_rows(i: int) -> int:
+    """Nordsieck rows the variant keeps in Tensor Memory (0: none)."""
+    return max(0, lib().qtm_variant_tmem_rows(i))
 
 
 def fp64_peak_tflops(device: int = 0) -> float:

@@ -89,7 +89,7 @@ def _self_sensitivity(oracle_lib, pk, n, stream="philox", begin=0):
 @pytest.mark.parametrize("name,n,variant", [("c1", 500, -1), ("c1", 500, 0), ("c2", 512, -1),
                                             ("c2", 512, 17),
                                             ("c3", 256, -1), ("c3", 256, 12),
-                                            ("c4", 256, -1), ("c4", 256, 6),
+                                            ("c4", 256, -1), ("c4", 256, 6), ("c4", 256, 39),
                                             ("c5", 256, -1), ("c5", 256, 15), ("c5", 256, 27)])
 def test_device_matches_oracle_identical_streams(name, n, variant, oracle_lib):
     """Identical streams, sample of n trajectories: jump counts and channels
@@ -348,3 +348,20 @@ def test_full_size_c5(oracle_lib):
     live = se > 1e-9
     z = np.abs(mean - ref["values"].mean(axis=0))[live] / se[live]
     assert np.mean(z > 3) < 0.02 and z.max() < 5
+
+
+def test_block_partials_reassemble_the_sums_bitwise():
+    # the multi-GPU reduction (engine.run_sharded): block-aligned shards'
+    # block partials, combined in block order on the host, are the
+    # single-run sums bit for bit
+    p = configs.build("c2")
+    n = 1000
+    with DeviceProblem(p) as dp:
+        full = dp.run(5, 0, n, per_trajectory=False, resident=True)
+        parts = [dp.run(5, b, e, per_trajectory=False, resident=True, block_sums=True)
+                 for b, e in (engine.shard_range(n, 3, r) for r in range(3))]
+    bs = np.concatenate([o.block_sum for o in parts])
+    bs2 = np.concatenate([o.block_sumsq for o in parts])
+    s, s2 = engine.combine_blocks(bs, bs2)
+    np.testing.assert_array_equal(s, full.sum)
+    np.testing.assert_array_equal(s2, full.sumsq)

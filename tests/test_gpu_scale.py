@@ -69,6 +69,11 @@ def test_identical_streams_vs_reference_at_scale(name, kind, oracle_lib, capsys)
         if m:
             worst_t = max(worst_t, float(np.abs(out.jump_t[i, :m] - s.jump_t[i]).max()))
         worst_v = max(worst_v, float(np.abs(out.values[i] - s.values[i]).max()))
+    dmean = float(np.abs(out.values[ok].mean(axis=0) - s.values[ok].mean(axis=0)).max())
+    with capsys.disabled():
+        print(f"\n[{name} {kind}, {n} trajectories, {int((~ok).sum())} reference failures] "
+              f"device vs reference: max |dt*| {worst_t:.2e}, max |dvalue| {worst_v:.2e}, "
+              f"max |dmean| {dmean:.2e}")
     assert worst_t <= tol_t, worst_t
     assert worst_v <= tol_v, worst_v
     # psi(t_j) itself for the first trajectories (north_star "psi(t) within 1e-6")
