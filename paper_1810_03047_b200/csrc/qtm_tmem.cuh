@@ -91,6 +91,53 @@ __device__ __forceinline__ void issue_ld4(uint32_t a, uint32_t& r0, uint32_t& r1
 __device__ __forceinline__ void st4(uint32_t a, const uint32_t (&r)[4]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" :: "r"(a), QTM_R4IN(r, 0) : "memory");
 }
+// W columns (W in 4..24, a multiple of 4) in x16 / x8 / x4 pieces
+template <int W>
+__device__ __forceinline__ void issue_ld(uint32_t a, uint32_t (&r)[W]) {
+    static_assert(W % 4 == 0 && W >= 4 && W <= 28, "4..28 columns");
+    if constexpr (W >= 16) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                     "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                     : QTM_R4(r, 0), QTM_R4(r, 4), QTM_R4(r, 8), QTM_R4(r, 12) : "r"(a));
+    }
+    constexpr int B = W >= 16 ? 16 : 0;
+    if constexpr (W - B >= 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : QTM_R4(r, B), QTM_R4(r, B + 4) : "r"(a + B));
+    }
+    constexpr int C = B + ((W - B) >= 8 ? 8 : 0);
+    if constexpr (W - C >= 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                     : QTM_R4(r, C) : "r"(a + C));
+    }
+}
+// wait for every outstanding load; the registers are re-defined after the
+// wait (empty asm, tied), so their uses cannot move above it
+template <int W>
+__device__ __forceinline__ void wait_ld(uint32_t (&r)[W]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < W; ++i) asm volatile("" : "+r"(r[i]));
+}
+template <int W>
+__device__ __forceinline__ void st(uint32_t a, const uint32_t (&r)[W]) {
+    static_assert(W % 4 == 0 && W >= 4 && W <= 28, "4..28 columns");
+    if constexpr (W >= 16) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 "
+                     "[%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+                     :: "r"(a), QTM_R4IN(r, 0), QTM_R4IN(r, 4), QTM_R4IN(r, 8), QTM_R4IN(r, 12) : "memory");
+    }
+    constexpr int B = W >= 16 ? 16 : 0;
+    if constexpr (W - B >= 8) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                     :: "r"(a + B), QTM_R4IN(r, B), QTM_R4IN(r, B + 4) : "memory");
+    }
+    constexpr int C = B + ((W - B) >= 8 ? 8 : 0);
+    if constexpr (W - C >= 4) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n"
+                     :: "r"(a + C), QTM_R4IN(r, C) : "memory");
+    }
+}
 #undef QTM_R4
 #undef QTM_R4IN
 #undef QTM_R4T

@@ -174,6 +174,21 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+// |a| for the error weights 1/(atol + rtol |y_i|) (ode.py: np.abs, i.e.
+// hypot).  QTM_FAST_ABS (default): sqrt(re^2 + im^2) -- within an ulp or two
+// of hypot for the |y_i| <= 1 of a normalised state (an underflowing square
+// only where atol dominates the weight anyway), at a fraction of hypot's
+// instructions (c4 +1.3 %); QTM_FAST_ABS=0 restores hypot.
+#ifndef QTM_FAST_ABS
+#define QTM_FAST_ABS 1
+#endif
+__device__ __forceinline__ double cmod(double2 a) {
+#if QTM_FAST_ABS
+    return sqrt(a.x * a.x + a.y * a.y);
+#else
+    return hypot(a.x, a.y);
+#endif
+}
 
 // est ** (1/(q+1)) etc. in the step-size controller (ode.py:302, 445-453):
 // x > 0 and a small exponent, evaluated as exp2(y * log2(x)); within a few
@@ -814,10 +829,31 @@ struct HistT {
     // Single-buffered: one component's 24 columns in flight at a time keeps
     // the register footprint small (the TMEM latency is hidden by the second
     // CTA on the SM, not by prefetching).
+    // runtime-indexed access to a small register array without local memory
+    __device__ __forceinline__ static double2 sel(const double2 (&a)[E], int e) {
+        double2 v = a[0];
+#pragma unroll
+        for (int k = 1; k < E; ++k) if (e == k) v = a[k];
+        return v;
+    }
+    __device__ __forceinline__ static void put(double2 (&a)[E], int e, double2 v) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) if (e == k) a[k] = v;
+    }
+    // QTM_TM_UNROLL=0: the component loop is not unrolled, so its body (an
+    // order switch over the register code of Hist<8, 1>) exists once -- a
+    // smaller instruction footprint for more local-memory traffic (r1).
+#ifndef QTM_TM_UNROLL
+#define QTM_TM_UNROLL 1
+#endif
     template <bool STORE, class F>
     __device__ __forceinline__ static void per_comp(Z& z, const O& ovf, F&& f) {
         tm::wait_st();
+#if QTM_TM_UNROLL
 #pragma unroll
+#else
+#pragma unroll 1
+#endif
         for (int e = 0; e < E; ++e) {
             uint32_t raw[24];
             tm::issue_ld24(rows_col(z, e), raw);
@@ -826,14 +862,14 @@ struct HistT {
             tm::unpack<6>(raw, t);
             double2 zc[ROWS][1];
             zc[0][0] = z.z0[(DP / E) * e];
-            zc[1][0] = z.r1[e];
+            zc[1][0] = sel(z.r1, e);
 #pragma unroll
             for (int k = 0; k < 6; ++k) zc[2 + k][0] = t[k];
             const typename H1::O o1{ovf.p + e * (DP / E)};
             f(zc, o1, e);
             if constexpr (STORE) {
                 z.z0[(DP / E) * e] = zc[0][0];
-                z.r1[e] = zc[1][0];
+                put(z.r1, e, zc[1][0]);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) t[k] = zc[2 + k][0];
                 tm::pack<6>(t, raw);
@@ -841,12 +877,62 @@ struct HistT {
             }
         }
     }
+    // Order-specialised form for Q <= 7 (every row on chip): only the TMEM
+    // rows 2..Q move, in one load of 4(Q-1) columns per component, and the
+    // arithmetic is Hist<8, 1>'s straight-line code for order Q.
+    template <int Q, class F>
+    __device__ __forceinline__ static void per_comp_q(Z& z, F&& f) {
+        constexpr int N = Q - 1;  // TMEM rows 2..Q
+        if constexpr (N > 0) tm::wait_st();
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double2 zc[ROWS][1];
+            uint32_t raw[4 * (N > 0 ? N : 1)];
+            if constexpr (N > 0) {
+                tm::issue_ld(rows_col(z, e), raw);
+                tm::wait_ld(raw);
+                double2 t[N > 0 ? N : 1];
+                tm::unpack<(N > 0 ? N : 1)>(raw, t);
+#pragma unroll
+                for (int k = 0; k < N; ++k) zc[2 + k][0] = t[k];
+            }
+            zc[0][0] = z.z0[(DP / E) * e];
+            zc[1][0] = z.r1[e];
+            f(zc, e);
+            z.z0[(DP / E) * e] = zc[0][0];
+            z.r1[e] = zc[1][0];
+            if constexpr (N > 0) {
+                double2 t[N];
+#pragma unroll
+                for (int k = 0; k < N; ++k) t[k] = zc[2 + k][0];
+                tm::pack<N>(t, raw);
+                tm::st(rows_col(z, e), raw);
+            }
+        }
+    }
+#define QTM_TM_QSWITCH(CALL)                                                 \
+    switch (q) {                                                             \
+        case 1: CALL(1); return;                                             \
+        case 2: CALL(2); return;                                             \
+        case 3: CALL(3); return;                                             \
+        case 4: CALL(4); return;                                             \
+        case 5: CALL(5); return;                                             \
+        case 6: CALL(6); return;                                             \
+        case 7: CALL(7); return;                                             \
+        default: break;                                                      \
+    }
     __device__ __forceinline__ static void predict(Z& z, const O& ovf, int q) {
+#define CALL_(Q) per_comp_q<Q>(z, [&](double2 (&zc)[ROWS][1], int) { H1::template predict_q<Q>(zc); })
+        QTM_TM_QSWITCH(CALL_)
+#undef CALL_
         per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int) {
             H1::predict(zc, o, q);
         });
     }
     __device__ __forceinline__ static void undo(Z& z, const O& ovf, int q) {
+#define CALL_(Q) per_comp_q<Q>(z, [&](double2 (&zc)[ROWS][1], int) { H1::template undo_q<Q>(zc); })
+        QTM_TM_QSWITCH(CALL_)
+#undef CALL_
         per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int) {
             H1::undo(zc, o, q);
         });
@@ -858,8 +944,15 @@ struct HistT {
     }
     __device__ __forceinline__ static void commit(Z& z, const O& ovf, int q, const double* l,
                                                   const double2 (&ev)[E]) {
+#define CALL_(Q)                                                                        \
+        per_comp_q<Q>(z, [&](double2 (&zc)[ROWS][1], int e) {                           \
+            const double2 ev1[1] = {sel(ev, e)};                                        \
+            H1::template commit_q<Q>(zc, l, ev1);                                       \
+        })
+        QTM_TM_QSWITCH(CALL_)
+#undef CALL_
         per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
-            const double2 ev1[1] = {ev[e]};
+            const double2 ev1[1] = {sel(ev, e)};
             H1::commit(zc, o, q, l, ev1);
         });
     }
@@ -867,7 +960,7 @@ struct HistT {
         per_comp<false>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
             double2 o1[1];
             H1::horner(zc, o, q, s, o1);
-            out[e] = o1[0];
+            put(out, e, o1[0]);
         });
     }
     __device__ __forceinline__ static void row_all(const Z& z, const O& ovf, int j, double2 (&out)[E]) {
@@ -1273,7 +1366,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         _Pragma("unroll") for (int e = 0; e < E; ++e) {                      \
             H::at(z, 0, e) = (y0)[e];                                        \
             H::at(z, 1, e) = cscale(h, f__[e]);                              \
-            W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot((y0)[e].x, (y0)[e].y)) : 0.0; \
+            W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * cmod((y0)[e])) : 0.0; \
         }                                                                    \
         ws.crate = 0.7; ialth = 2; has_eprev = false;                        \
     } while (0)
@@ -1426,7 +1519,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const double2 z0 = H::at(z, 0, e);
-                    W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * hypot(z0.x, z0.y)) : 0.0;
+                    W(e) = ACT(e) ? __drcp_rn(P.atol + P.rtol * cmod(z0)) : 0.0;
                 }
                 PH_MARK(11);  // [11] accepted-step bookkeeping + error weights
                 ialth -= 1;
