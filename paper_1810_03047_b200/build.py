@@ -72,7 +72,7 @@ VARIANTS = [
     (128, 1, 0, 6, 0),       # 20
     (32, 1, 0, 32, 0),       # 21
     # one CTA per SM with fewer, wider threads: up to 255 registers each
-    (256, 4, 8, 1, 1024),    # 22 automatic for 512 < d <= 1024 (c4 1.44x, c5 1.19x faster than #6)
+    (256, 4, 8, 1, 0),       # 22 (automatic for 512 < d <= 1024 before #39: c4 1.44x, c5 1.19x faster than #6)
     (256, 4, 10, 1, 0),      # 23
     (256, 4, 6, 1, 0),       # 24
     (128, 8, 5, 1, 0),       # 25
@@ -98,7 +98,7 @@ VARIANTS = [
     # Nordsieck rows 2..7 and e / e_prev in TMEM (HistT, csrc/qtm_tmem.cuh):
     # 128 registers and ~110 KB of shared memory per d <= 1024 trajectory,
     # so two trajectory CTAs share an SM (each allocating 256 TMEM columns)
-    (256, 4, 8, 2, 0, False, True),   # 39
+    (256, 4, 8, 2, 1024, False, True),   # 39  automatic for 512 < d <= 1024 (c4 1.21x over #22)
 ]
 
 SOURCES = ["qtm_traj.cuh", "qtm_bdf.cuh", "qtm_rng.cuh", "qtm_capi.cu"]

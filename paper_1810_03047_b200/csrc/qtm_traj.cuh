@@ -1062,11 +1062,13 @@ struct TrajKernel {
 // TD: variant compiled with the time-dependent generator terms (td_apply
 // calls cost registers even when not taken, so constant-generator variants
 // are built without them)
-// Register cap of the TMEM variants: two 256-thread CTAs per SM need less
-// than the 128 registers __launch_bounds__(256, 2) allows (measured: at 128
-// the occupancy calculator grants one CTA per SM)
+// Register cap of the TMEM variants: 128 (what __launch_bounds__(256, 2)
+// allows; two CTAs per SM do co-reside -- the runtime's occupancy calculator
+// claims otherwise for tcgen05 kernels, see variant_occupancy in
+// qtm_capi.cu).  Measured on c4: 112 -> 29.2k, 120 -> 33.0k, 128 -> 35.4k
+// trajectories/s.
 #ifndef QTM_TM_MAXNREG
-#define QTM_TM_MAXNREG 120
+#define QTM_TM_MAXNREG 128
 #endif
 #define QTM_MAXNREG(NT, MINB, TM) __maxnreg__((TM) ? QTM_TM_MAXNREG : 65536 / ((NT) * (MINB)) > 255 ? 255 : 65536 / ((NT) * (MINB)))
 // TM: Nordsieck rows 2..7 and the e buffers in TMEM (HistT; RREG must be 8,
