@@ -464,7 +464,8 @@ def main(argv=None):
                                           if outs[-1].variant >= 0 else "bdf_kernel"),
                        "grid_ctas": outs[-1].grid,
                        "history_rows": {"registers": layout["reg_rows"],
-                                        "shared": layout["smem_rows"]},
+                                        "shared": layout["smem_rows"],
+                                        "tmem": layout.get("tmem_rows", 0)},
                        "smem_per_cta": layout["smem_bytes"]},
             "e2e": {"value": e2e_value, "unit": "trajectories/s",
                     "h2d_bytes_per_step": int(packed.nbytes()), "d2h_bytes_per_step": int(d2h)},
