@@ -203,6 +203,10 @@ int qtm_variant_time_dependent(int i);
 /* Nordsieck rows variant i keeps in Tensor Memory (rows 2..7 with the e
  * buffers: 6), 0 for register / shared-memory histories, < 0 on a bad index */
 int qtm_variant_tmem_rows(int i);
+/* one-thread-per-trajectory variants (csrc/qtm_small.cuh): the largest
+ * state dimension (0 for the CTA-per-trajectory variants) and the
+ * trajectories sharing a warp */
+int qtm_variant_small(int i, int32_t* d_max, int32_t* lanes);
 /* kernel variant a problem runs (-1: the BDF kernel) */
 int qtm_problem_variant(qtm_problem* problem);
 int qtm_device_count(void);

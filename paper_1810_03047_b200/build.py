@@ -100,8 +100,18 @@ VARIANTS = [
     # so two trajectory CTAs share an SM (each allocating 256 TMEM columns)
     (256, 4, 8, 2, 1024, False, True),   # 39  automatic for 512 < d <= 1024 (c4 1.21x over #22)
 ]
+# one thread per trajectory for tiny states (csrc/qtm_small.cuh):
+# (d_max, trajectories per warp, auto-select for dim <= this (0 = never))
+# c1 (500 trajectories, ~220 strictly sequential attempts each) measured per
+# step: (32,1,13) 1.09 ms; (2, 1 lane) 0.75 ms; (2, 4 lanes) 1.13 ms;
+# (2, 32 lanes) 1.93 ms (divergence); (4, 1) 1.52 ms
+SMALL_VARIANTS = [
+    (2, 1, 2),     # 40  automatic for d <= 2 (c1)
+    (2, 4, 0),     # 41  (more trajectories per warp: large ensembles)
+    (4, 1, 4),     # 42  automatic for 2 < d <= 4
+]
 
-SOURCES = ["qtm_traj.cuh", "qtm_bdf.cuh", "qtm_rng.cuh", "qtm_capi.cu"]
+SOURCES = ["qtm_traj.cuh", "qtm_bdf.cuh", "qtm_rng.cuh", "qtm_tmem.cuh", "qtm_small.cuh", "qtm_capi.cu"]
 
 
 def nvcc() -> str:
@@ -137,7 +147,25 @@ VariantDesc variant_{i}() {{
     return VariantDesc{{{nt}, {e}, {rr}, {mb}, {auto}, {1 if td == "true" else 0},
                        TrajKernel<{nt}, {e}, {rr}, {tmem}>::smem_bytes(),
                        reinterpret_cast<const void*>(traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>),
-                       {1 if tmem == "true" else 0}}};
+                       {1 if tmem == "true" else 0}, 0, 0}};
+}}
+}}  // namespace qtm
+"""
+        _write_if_changed(os.path.join(GEN, name), body)
+        files.append(os.path.join(GEN, name))
+        decls.append(f"VariantDesc variant_{i}();")
+        rows.append(f"        variant_{i}(),")
+    for j, (dmax, lanes, auto) in enumerate(SMALL_VARIANTS):
+        i = len(VARIANTS) + j
+        name = f"variant_{i}.cu"
+        body = f"""// generated by build.py -- kernel variant {i} (one thread per trajectory)
+#include "../qtm_small.cuh"
+namespace qtm {{
+template __global__ void traj1_kernel<{dmax}>(const __grid_constant__ DevProblem,
+                                            const __grid_constant__ RunParams);
+VariantDesc variant_{i}() {{
+    return VariantDesc{{128, {dmax}, 13, 1, {auto}, 0, 0,
+                       reinterpret_cast<const void*>(traj1_kernel<{dmax}>), 0, {dmax}, {lanes}}};
 }}
 }}  // namespace qtm
 """
@@ -159,6 +187,7 @@ def _stamp(paths) -> str:
         h.update(open(p, "rb").read())
     h.update(" ".join(NVCC_FLAGS).encode())
     h.update(repr(VARIANTS).encode())
+    h.update(repr(SMALL_VARIANTS).encode())
     return h.hexdigest()
 
 

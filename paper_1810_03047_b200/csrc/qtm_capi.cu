@@ -22,6 +22,7 @@
 #include "../../include/qtm.h"
 #include "qtm_traj.cuh"
 #include "qtm_bdf.cuh"
+#include "qtm_small.cuh"
 
 using namespace qtm;
 
@@ -148,6 +149,7 @@ struct Variant {
     size_t smem;
     const void* fn;
     int tm;  // history rows 2..7 + e buffers in TMEM (HistT)
+    int small, lanes;  // traj1_kernel: one thread per trajectory for d <= small, `lanes` per warp
     // TMEM columns per CTA (tm only): 32 per component and thread, per lane
     // quarter of warps
     int tmem_cols() const { return tm ? (threads / 128) * 32 * comps : 0; }
@@ -164,7 +166,7 @@ const std::vector<Variant>& variants() {
         std::vector<Variant> out;
         for (const qtm::VariantDesc& d : qtm_variant_table())
             out.push_back(Variant{d.threads, d.comps, d.reg_rows, d.min_blocks, d.auto_upto, d.td, d.smem, d.fn,
-                                  d.tm});
+                                  d.tm, d.small, d.lanes});
         return out;
     }();
     return v;
@@ -626,6 +628,14 @@ int qtm_problem_variant(qtm_problem* p) {
     return p->method == 1 ? -1 : p->variant;
 }
 
+int qtm_variant_small(int i, int32_t* d_max, int32_t* lanes) {
+    if (i < 0 || i >= (int)variants().size() || !d_max || !lanes)
+        return set_error(QTM_ERR_ARGS, "variant index out of range / null output");
+    *d_max = variants()[i].small;
+    *lanes = variants()[i].lanes;
+    return QTM_OK;
+}
+
 int qtm_variant_tmem_rows(int i) {
     if (i < 0 || i >= (int)variants().size()) return set_error(QTM_ERR_ARGS, "variant index out of range");
     return variants()[i].tm ? 6 : 0;
@@ -667,7 +677,7 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     const Variant& var = variants()[variant];
     if (d->method == 0 && d->n_td > 0 && !var.td)
         return set_error(QTM_ERR_ARGS, "kernel variant built without time-dependent terms");
-    if (d->method == 0 && (int64_t)var.threads * var.comps < d->dim)
+    if (d->method == 0 && (var.small ? (int64_t)var.small : (int64_t)var.threads * var.comps) < d->dim)
         return set_error(QTM_ERR_ARGS, "kernel variant too small for this dimension");
 
     qtm_problem* p = new qtm_problem();
@@ -790,14 +800,34 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         if (cudaFuncSetAttribute(p->bdf_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bcap) != cudaSuccess)
             rc = set_error(QTM_ERR_CUDA, "cudaFuncSetAttribute(max dynamic smem, BDF) failed");
     }
-    if (rc == QTM_OK && p->method == 0) {
+    if (rc == QTM_OK && p->method == 0 && var.small) {
+        // dense [op][i][j] blocks padded to d_max (CSR columns are strictly
+        // increasing, so each entry is one CSR value)
+        const int dm = var.small;
+        const int nops = 1 + d->n_collapse + d->n_expect;
+        std::vector<double2> ops((size_t)nops * dm * dm, make_double2(0.0, 0.0));
+        auto put = [&](int k, const qtm_csr& m) {
+            for (int64_t i = 0; i < d->dim; ++i)
+                for (int64_t j = m.row_ptr[i]; j < m.row_ptr[i + 1]; ++j)
+                    ops[((size_t)k * dm + i) * dm + m.col_ind[j]] = make_double2(m.values[2 * j], m.values[2 * j + 1]);
+        };
+        put(0, d->generator);
+        for (int c = 0; c < d->n_collapse; ++c) put(1 + c, d->collapse[c]);
+        for (int k = 0; k < d->n_expect; ++k) put(1 + d->n_collapse + k, d->expect[k]);
+        double2* dops = nullptr;
+        if (upload(p, &dops, ops.data(), ops.size()) != cudaSuccess)
+            rc = set_error(QTM_ERR_CUDA, "upload of the dense operators failed");
+        P.small_ops = dops;
+        p->smem = sizeof(double2) * ops.size();
+    }
+    if (rc == QTM_OK && p->method == 0 && !var.small) {
         bool staged = false;
         std::vector<const qtm_csr*> tds;
         if (var.td)
             for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds);
     }
-    if (rc == QTM_OK && p->method == 0) rc = build_expect_diag(p, d, var.threads * var.comps);
+    if (rc == QTM_OK && p->method == 0 && !var.small) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->method == 0 && var.tm) {
         // every resident CTA allocates tmem_cols() of the SM's 512 TMEM
         // columns (variant_occupancy counts them); the hardware must never
@@ -843,7 +873,8 @@ int qtm_max_resident(qtm_problem* p, int32_t* ctas) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p->bdf_fn, p->bdf_threads, p->smem));
     else
         CUDA_TRY(variant_occupancy(var, p->smem, p->device, &per_sm));
-    *ctas = sms * per_sm;
+    // (one thread per trajectory: trajectories in flight, not CTAs)
+    *ctas = sms * per_sm * (p->method == 0 && var.small ? (var.threads / 32) * var.lanes : 1);
     return QTM_OK;
 }
 
@@ -859,6 +890,8 @@ int qtm_problem_layout(qtm_problem* p, int32_t* reg_rows, int32_t* smem_rows, in
     *smem_bytes = (int64_t)p->smem;
     return QTM_OK;
 }
+
+constexpr long long kRunChunkMax = 1ll << 16;  // trajectories per launch chunk
 
 static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool copy_per_traj) {
     if (!p || !a || !o) return set_error(QTM_ERR_ARGS, "null argument");
@@ -899,6 +932,9 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     else CUDA_TRY(variant_occupancy(var, p->smem, p->device, &per_sm));
     if (per_sm < 1) return set_error(QTM_ERR_CUDA, "kernel variant cannot be resident (registers/smem)");
     long long grid = std::min<long long>((long long)dev_sms * per_sm, std::min<long long>(count, 1ll << 16));
+    const bool small = !bdf && var.small > 0;
+    const int per_cta = small ? (kthreads / 32) * var.lanes : 1;  // trajectories per CTA
+    if (small) grid = (std::min<long long>(count, kRunChunkMax) + per_cta - 1) / per_cta;
     if (bdf && !p->bdf_in_smem) {
         // HBM workspaces (d^2 LU per CTA): at most ~8 GB of them, >= 1 per SM
         const long long cap = std::max<long long>(dev_sms, (8ll << 30) / (16ll * p->bdf_ws_elems));
@@ -912,10 +948,10 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     // would otherwise need ~8 GB of partial sums).  kRunChunk is a multiple
     // of the 256-trajectory reduction block, so the fixed-order ensemble sum
     // is the same as for one launch.
-    constexpr long long kRunChunk = 1ll << 16;
+    constexpr long long kRunChunk = kRunChunkMax;
     constexpr int kRedChunk = QTM_BLOCK;
     const long long run_chunk = std::min<long long>(count, kRunChunk);
-    const int nw = kthreads / 32;
+    const int nw = small ? 1 : kthreads / 32;  // recording partials per point
     const int DP = var.threads * var.comps;
     const long long n_red_total = (count + kRedChunk - 1) / kRedChunk;
     CUDA_TRY(p->values.ensure((size_t)run_chunk * std::max(n_out, 1), s));
@@ -975,7 +1011,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
 
     for (long long off = 0; off < count; off += kRunChunk) {
         const long long cnt = std::min<long long>(kRunChunk, count - off);
-        const long long cgrid = std::min<long long>(grid, cnt);
+        const long long cgrid = small ? (cnt + per_cta - 1) / per_cta : std::min<long long>(grid, cnt);
         // ctl = {work counter 0, first failing row ~0, phase counters 0}
         CUDA_TRY(cudaMemsetAsync(p->ctl.p, 0, sizeof(unsigned long long) * 18, s));
         CUDA_TRY(cudaMemsetAsync(p->ctl.p + 1, 0xFF, sizeof(unsigned long long), s));
@@ -1005,6 +1041,7 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         R.psi_slot = want_psi ? p->psi_slot.p : nullptr;
         R.psi_out = want_psi ? p->psi_out.p : nullptr;
         R.n_psi = want_psi ? a->n_psi_points : 0;
+        R.lanes = small ? var.lanes : 0;
         BdfParams BP{};
         BP.ws = p->bdf_ws.p;
         BP.ws_stride = p->bdf_ws_elems;

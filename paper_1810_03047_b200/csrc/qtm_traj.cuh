@@ -58,7 +58,9 @@ struct VariantDesc {
     int threads, comps, reg_rows, min_blocks, auto_upto, td;
     size_t smem;
     const void* fn;
-    int tm;  // Nordsieck rows 2..7 and e / e_prev in TMEM (HistT)
+    int tm;     // Nordsieck rows 2..7 and e / e_prev in TMEM (HistT)
+    int small;  // one thread per trajectory for d <= small (traj1_kernel, qtm_small.cuh); 0: no
+    int lanes;  // small: trajectories per warp
 };
 
 struct DevCsr {
@@ -115,6 +117,9 @@ struct DevProblem {
     // diagonal [ne][DP] (doubles, copied from e_dense_g) instead of bytes
     int e_fast, e_stage_dense;
     const double* e_dense_g;
+    // small-state kernel (traj1_kernel): G, C_k, E_k as dense [d_max][d_max]
+    // blocks, [1 + nc + ne][d_max][d_max]
+    const double2* small_ops;
     double l[LROWS][LROWS];
     double tau1[LROWS], tau2[LROWS], tau3[LROWS];
     // per-order constants the reference evaluates inline, tabulated on the
@@ -157,6 +162,7 @@ struct RunParams {
     unsigned long long* counter;
     unsigned long long* first_fail;  // atomicMin over failing rows
     unsigned long long* phase_cycles;  // [16] (QTM_PHASES builds only)
+    int lanes;               // traj1_kernel: trajectories per warp
     // psi snapshots (diagnostics / parity): slot of each grid index (-1 =
     // none; nullptr = no snapshots) and the output [n_traj][n_psi][d]
     const int* psi_slot;

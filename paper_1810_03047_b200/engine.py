@@ -316,12 +316,19 @@ def candidate_variants(dim: int, time_dependent: bool = False) -> list[int]:
     wasting more than half of their lanes (the smallest fit always counts),
     among those built with / without the time-dependent terms."""
     vs = native.variants()
+    small = [i for i in range(len(vs)) if 0 < native.variant_small(i)[0]]
     fits = [i for i, (t, e, _) in enumerate(vs)
-            if t * e >= dim and native.variant_time_dependent(i) == time_dependent]
-    if not fits:
-        return []
-    smallest = min(vs[i][0] * vs[i][1] for i in fits)
-    return [i for i in fits if vs[i][0] * vs[i][1] <= max(2 * dim, smallest)]
+            if i not in small and t * e >= dim
+            and native.variant_time_dependent(i) == time_dependent]
+    cands = []
+    if fits:
+        smallest = min(vs[i][0] * vs[i][1] for i in fits)
+        cands = [i for i in fits if vs[i][0] * vs[i][1] <= max(2 * dim, smallest)]
+    # one thread per trajectory (constant generators only): the smallest d_max >= dim
+    dms = [native.variant_small(i)[0] for i in small if native.variant_small(i)[0] >= dim]
+    if dms and not time_dependent:
+        cands += [i for i in small if native.variant_small(i)[0] == min(dms)]
+    return cands
 
 
 def autotune_variant(packed: PackedProblem, *, device: int = 0, sample: int | None = None,

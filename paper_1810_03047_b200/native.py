@@ -86,7 +86,7 @@ EXPORTS = ("qtm_problem_create", "qtm_run", "qtm_run_resident", "qtm_problem_des
            "qtm_last_error", "qtm_abi_version", "qtm_num_variants", "qtm_variant_info",
            "qtm_device_count", "qtm_measure_fp64_peak", "qtm_phase_cycles",
            "qtm_variant_time_dependent", "qtm_measure_dmma_peak", "qtm_variant_tmem_rows",
-           "qtm_problem_variant")
+           "qtm_problem_variant", "qtm_variant_small")
 
 _lib = None
 
@@ -127,6 +127,8 @@ def lib():
     L.qtm_variant_info.restype = C.c_int
     L.qtm_variant_time_dependent.argtypes = [C.c_int]
     L.qtm_variant_time_dependent.restype = C.c_int
+    L.qtm_variant_small.argtypes = [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.qtm_variant_small.restype = C.c_int
     L.qtm_problem_variant.argtypes = [C.c_void_p]
     L.qtm_problem_variant.restype = C.c_int
     L.qtm_variant_tmem_rows.argtypes = [C.c_int]
@@ -170,6 +172,15 @@ def dmma_peak_tflops(device: int = 0) -> float:
 
 def variant_time_dependent(i: int) -> bool:
     return lib().qtm_variant_time_dependent(i) == 1
+
+
+def variant_small(i: int) -> tuple[int, int]:
+    """(d_max, trajectories per warp) of a one-thread-per-trajectory variant,
+    (0, 0) for the CTA-per-trajectory variants."""
+    dm, ln = C.c_int32(), C.c_int32()
+    if lib().qtm_variant_small(i, C.byref(dm), C.byref(ln)) != 0:
+        raise RuntimeError(last_error())
+    return dm.value, ln.value
 
 
 def variant_tmem_rows(i: int) -> int:

@@ -86,7 +86,8 @@ def _self_sensitivity(oracle_lib, pk, n, stream="philox", begin=0):
 # others are the autotune's picks for c5 (192x5, 4 register rows, two CTAs
 # per SM; 256x4 was an earlier pick), c3 (96x1, 9 rows), c2 (32x1, history
 # in smem), c1 (32x1, 13 register rows) and c4's previous default (512x2)
-@pytest.mark.parametrize("name,n,variant", [("c1", 500, -1), ("c1", 500, 0), ("c2", 512, -1),
+@pytest.mark.parametrize("name,n,variant", [("c1", 500, -1), ("c1", 500, 0), ("c1", 500, 41),
+                                            ("c1", 500, 42), ("c2", 512, -1),
                                             ("c2", 512, 17),
                                             ("c3", 256, -1), ("c3", 256, 12),
                                             ("c4", 256, -1), ("c4", 256, 6), ("c4", 256, 39),
@@ -193,7 +194,8 @@ def _observable_mix(kind):
 
 
 @pytest.mark.parametrize("kind", ["real_diag", "off_diag", "complex_diag"])
-@pytest.mark.parametrize("variant", [0, 17])  # register history / shared-memory history
+# register history / shared-memory history / one thread per trajectory
+@pytest.mark.parametrize("variant", [0, 17, 40, 42])
 def test_recording_paths_match_oracle(kind, variant, oracle_lib):
     pk = pack_problem(_observable_mix(kind))
     with DeviceProblem(pk, variant=variant) as dp:

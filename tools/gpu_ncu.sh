@@ -5,7 +5,7 @@ cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
 TAG=$1; CFG=${2:-c4}; NT=${3:-1184}; V=$4
 CMD="python bench.py --config $CFG --trajectories $NT --steps 1 --warmup 3 --no-cpu ${V:+--variant $V}"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:traj_kernel -s 3 -c 1 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"traj_kernel|traj1_kernel" -s 3 -c 1 \
     -o gpurun_out/${TAG} $CMD > gpurun_out/${TAG}_ncu.log 2>&1
 echo "rc=$?" >> gpurun_out/${TAG}_ncu.log
 if [ -f gpurun_out/${TAG}.ncu-rep ]; then
