@@ -182,10 +182,10 @@ CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1, "c4td"
 def profiled_traffic(config: str):
     """DRAM bytes per launch of the trajectory kernel from the newest committed
     ncu --set full capture of this config
-    (profiles/r<NN>_<config>_traj_kernel_raw_selected.csv), or None."""
+    (profiles/r*_<config>_traj_kernel_raw_selected.csv, newest file), or None."""
     import glob
-    found = sorted(glob.glob(os.path.join(REPO, "profiles",
-                                          f"r[0-9][0-9]_{config}_traj_kernel_raw_selected.csv")))
+    found = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_{config}_traj_kernel_raw_selected.csv")),
+                   key=os.path.getmtime)
     if not found:
         return None
     path = found[-1]
@@ -225,6 +225,39 @@ def build_problem(args):
     return p
 
 
+REF_ENGINE_SAMPLE = {"c1": 2000, "c2": 160, "c3": 96, "c4": 128, "c5": 16, "c4td": 64}
+
+
+def reference_engine(config: str, workers: int):
+    """The reference's OWN CPU engine (Python + numba, pip-installed into
+    baseline/_ref) timed on this host: ``mcwf.run_local_farm`` (cluster.py:493)
+    over a bounded sample of the config, problem built by the reference's
+    constructors (tests/golden/ref_configs.py), numba compiled in the parent
+    before the fork (untimed).  None when the reference package is absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mcwf")) or config not in REF_ENGINE_SAMPLE \
+            or config == "c4td":
+        return None
+    sys.path.insert(0, os.path.join(REPO, "tests", "golden"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "qtm_numba"))
+    try:
+        import ref_configs  # noqa: F401  (puts baseline/_ref on sys.path)
+        import mcwf
+        from oracle.streams import PhiloxStream
+    except ImportError:
+        return None
+    problem = ref_configs.CONFIGS[config](log_jumps=False)
+    mcwf.run_single_trajectory(problem, PhiloxStream(SEED, 0))  # numba JIT, untimed
+    n = REF_ENGINE_SAMPLE[config]
+    t0 = time.perf_counter()
+    mcwf.run_local_farm(problem, n, workers, SEED)
+    sec = time.perf_counter() - t0
+    return {"value": n / sec, "unit": "trajectories/s", "cores": workers, "kind": "reference",
+            "sample": f"{n} trajectories of {config}: mcwf.run_local_farm(problem, {n}, {workers}, "
+                      f"{SEED}) from baseline/_ref (the reference's own Python + numba engine, "
+                      f"one worker process per host thread)"}
+
+
 def run_reference_arm(args, rank, world):
     from paper_1810_03047_b200.packing import pack_problem
     if rank != 0:
@@ -245,6 +278,11 @@ def run_reference_arm(args, rank, world):
                              "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": "trajectories/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if args.method == "adams":
+        try:
+            line["reference_engine"] = reference_engine(args.config, threads)
+        except Exception as exc:  # the port's line stands on its own
+            line["reference_engine"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     print(json.dumps(line), flush=True)
 
 

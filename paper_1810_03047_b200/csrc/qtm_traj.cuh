@@ -203,6 +203,27 @@ static __device__ __noinline__ double ctl_pow(double x, double y) {
     return x > 0.0 ? exp2(y * log2(x)) : (x == 0.0 ? 0.0 : pow(x, y));
 }
 
+// One complex multiply-accumulate of the staged SpMV, acc += v * x.  The
+// reference forms the product (ac - bd, ad + bc) and then adds it
+// (_kernels.py:18-26, numba complex_mul); QTM_CMAC_FMA accumulates the four
+// real products straight into the sum with FMAs instead -- the same terms
+// in the same column order, rounded at different points (~1 ulp per row of
+// G), 4 FP64 instructions per entry instead of 6.
+#ifndef QTM_CMAC_FMA
+#define QTM_CMAC_FMA 0
+#endif
+__device__ __forceinline__ void cmac(double& sr, double& si, double2 v, double2 x) {
+#if QTM_CMAC_FMA
+    sr = fma(v.x, x.x, sr);
+    sr = fma(-v.y, x.y, sr);
+    si = fma(v.x, x.y, si);
+    si = fma(v.y, x.x, si);
+#else
+    sr = sr + (v.x * x.x - v.y * x.y);
+    si = si + (v.x * x.y + v.y * x.x);
+#endif
+}
+
 // y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then
 // accumulated (reference _kernels.py:150-154, numba complex_mul).
 // not inlined: it serves the cold paths (recording of off-diagonal
@@ -266,8 +287,7 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
                 const uint32_t u = ent[off[e] + k * 32 + lane];
                 const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
                 const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
-                sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
-                si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
+                cmac(sr[e], si[e], v, xv);
             }
         }
     } else if constexpr (PF == 1) {
@@ -286,8 +306,7 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
             for (int e = 0; e < E; ++e) u[e] = ent[off[e] + kn * 32 + lane];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                sr[e] = sr[e] + (v[e].x * xv[e].x - v[e].y * xv[e].y);
-                si[e] = si[e] + (v[e].x * xv[e].y + v[e].y * xv[e].x);
+                cmac(sr[e], si[e], v[e], xv[e]);
             }
         }
     } else {
@@ -312,8 +331,7 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
             for (int e = 0; e < E; ++e) u[e] = ent[off[e] + k2 * 32 + lane];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                sr[e] = sr[e] + (v[e].x * xv[e].x - v[e].y * xv[e].y);
-                si[e] = si[e] + (v[e].x * xv[e].y + v[e].y * xv[e].x);
+                cmac(sr[e], si[e], v[e], xv[e]);
                 v[e] = vn[e];
                 xv[e] = xn[e];
             }
@@ -346,10 +364,8 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
             const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
             const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
             const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
-            sr[e] = sr[e] + (v.x * xv.x - v.y * xv.y);
-            si[e] = si[e] + (v.x * xv.y + v.y * xv.x);
-            tr[e] = tr[e] + (w.x * xv.x - w.y * xv.y);
-            ti[e] = ti[e] + (w.x * xv.y + w.y * xv.x);
+            cmac(sr[e], si[e], v, xv);
+            cmac(tr[e], ti[e], w, xv);
         }
     }
 #pragma unroll
@@ -377,8 +393,7 @@ __device__ __forceinline__ void sell_spmv_term(const uint32_t* __restrict__ ent,
             const int slot = off[e] + k * 32 + lane;
             const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
             const double2 xv = *reinterpret_cast<const double2*>(xb + (ent[slot] & 0xFFFFu));
-            tr[e] = tr[e] + (w.x * xv.x - w.y * xv.y);
-            ti[e] = ti[e] + (w.x * xv.y + w.y * xv.x);
+            cmac(tr[e], ti[e], w, xv);
         }
     }
 #pragma unroll
