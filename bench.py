@@ -182,10 +182,10 @@ CPU_SAMPLE_PER_THREAD = {"c1": 128, "c2": 32, "c3": 16, "c4": 8, "c5": 1, "c4td"
 def profiled_traffic(config: str):
     """DRAM bytes per launch of the trajectory kernel from the newest committed
     ncu --set full capture of this config
-    (profiles/r*_<config>_traj_kernel_raw_selected.csv, newest file), or None."""
+    (profiles/r*_<config>_traj_kernel_raw_selected.csv), or None."""
     import glob
-    found = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_{config}_traj_kernel_raw_selected.csv")),
-                   key=os.path.getmtime)
+    # round-1 captures are r0<N>_*, round 2's r2_*: the last name is the newest
+    found = sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_{config}_traj_kernel_raw_selected.csv")))
     if not found:
         return None
     path = found[-1]

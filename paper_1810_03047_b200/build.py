@@ -98,7 +98,9 @@ VARIANTS = [
     # Nordsieck rows 2..7 and e / e_prev in TMEM (HistT, csrc/qtm_tmem.cuh):
     # 128 registers and ~110 KB of shared memory per d <= 1024 trajectory,
     # so two trajectory CTAs share an SM (each allocating 256 TMEM columns)
-    (256, 4, 8, 2, 1024, False, True),   # 39  automatic for 512 < d <= 1024 (c4 1.21x over #22)
+    (256, 4, 8, 2, 1024, False, True),   # 39  automatic for 512 < d <= 1024 (c4 1.29x over #22)
+    # (its time-dependent twin needs 208 KB of shared memory for c4td's
+    # union-pattern tables, so one CTA per SM: 13.2k vs #36's 15.4k; not built)
 ]
 # one thread per trajectory for tiny states (csrc/qtm_small.cuh):
 # (d_max, trajectories per warp, auto-select for dim <= this (0 = never))

@@ -203,25 +203,14 @@ static __device__ __noinline__ double ctl_pow(double x, double y) {
     return x > 0.0 ? exp2(y * log2(x)) : (x == 0.0 ? 0.0 : pow(x, y));
 }
 
-// One complex multiply-accumulate of the staged SpMV, acc += v * x.  The
-// reference forms the product (ac - bd, ad + bc) and then adds it
-// (_kernels.py:18-26, numba complex_mul); QTM_CMAC_FMA accumulates the four
-// real products straight into the sum with FMAs instead -- the same terms
-// in the same column order, rounded at different points (~1 ulp per row of
-// G), 4 FP64 instructions per entry instead of 6.
-#ifndef QTM_CMAC_FMA
-#define QTM_CMAC_FMA 0
-#endif
+// acc += v * x: the product (ac - bd, ad + bc), then the sum, as the
+// reference's complex_mul + add (_kernels.py:18-26).  (Accumulating the four
+// real products straight into the sums with FMAs saves two FP64
+// instructions per entry but moved c4 jump times by 9e-6 against the
+// reference, and was no faster: measured, not kept.)
 __device__ __forceinline__ void cmac(double& sr, double& si, double2 v, double2 x) {
-#if QTM_CMAC_FMA
-    sr = fma(v.x, x.x, sr);
-    sr = fma(-v.y, x.y, sr);
-    si = fma(v.x, x.y, si);
-    si = fma(v.y, x.x, si);
-#else
     sr = sr + (v.x * x.x - v.y * x.y);
     si = si + (v.x * x.y + v.y * x.x);
-#endif
 }
 
 // y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then

@@ -66,10 +66,10 @@ def test_td_run_gpu_and_variant_guard(oracle_lib):
         DeviceProblem(g.problem, variant=plain)
 
 
-@pytest.mark.parametrize("variant", [-1, 36])
+@pytest.mark.parametrize("variant", [-1, 34, 36])
 def test_td_c4td_variants_match_oracle(variant, oracle_lib):
-    """c4td (bench workload): the automatic TD variant and the (256, 4, 8)
-    shape the autotune picks for it, vs the oracle."""
+    """c4td (bench workload): the automatic TD variant, the former default
+    (512, 2, 8) and the (256, 4, 8) shape the autotune picks, vs the oracle."""
     from paper_1810_03047_b200 import configs
     assert native.variant_time_dependent(36) and native.variant_time_dependent(37)
     pk = pack_problem(configs.build("c4td"))
