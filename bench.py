@@ -512,20 +512,22 @@ def main(argv=None):
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": (profiled_traffic(args.config) or {}).get("bytes"),
                          "traffic_source": (profiled_traffic(args.config) or {}).get("source"),
-                         "kernel": ("traj_kernel (persistent; state in registers/smem)"
+                         "kernel": (("traj1_kernel (one thread per trajectory; state in registers)"
+                                     if native.variant_small(outs[-1].variant)[0] else
+                                     "traj_kernel (persistent; Nordsieck rows 2..7 + e buffers in "
+                                     "TMEM, 2 CTAs/SM)" if layout.get("tmem_rows") else
+                                     "traj_kernel (persistent; state in registers/smem)")
                                     if args.method == "adams" else
                                     "bdf_kernel (persistent; LU + Newton in smem/HBM workspace)"),
                          "peak_source": "measured DFMA throughput on this GPU "
                                         "(qtm_measure_fp64_peak, 2 flops/DFMA)",
                          "flops_per_launch": flops, "kernel_ms": k_ms,
-                         "frac_of_unfused_ceiling": 2.0 * achieved / peak,
                          "dmma_peak_tflops": dmma_peak,
                          "dmma_note": "measured FP64 tensor-core (mma.sync m8n8k4 DMMA) "
                                       "throughput: the ceiling of a dense H_eff path",
-                         "unfused_note": "the arithmetic is deliberately unfused (-fmad=false, "
-                                         "the reference's numba kernels are not fast-math): "
-                                         "every flop is one DMUL/DADD instruction, so half "
-                                         "the DFMA figure is this code's FP64 ceiling",
+                         "build": ("fused multiply-add (QTM_FMAD=1, default)" if
+                                   os.environ.get("QTM_LIB", "").find("parity") < 0 else
+                                   "unfused parity build (QTM_FMAD=0)"),
                          "hbm_equiv_gbs": hbm_equiv,
                          "hbm_equiv_frac": hbm_equiv / hbm_peak if hbm_peak else None,
                          "hbm_peak_gbs": hbm_peak,
