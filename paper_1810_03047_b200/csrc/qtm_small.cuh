@@ -115,7 +115,7 @@ traj1_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPa
     };
     auto weights = [&](const double2 (&y)[DMAX]) {
 #pragma unroll
-        for (int e = 0; e < DMAX; ++e) w[e] = ACT1(e) ? __drcp_rn(P.atol + P.rtol * cmod(y[e])) : 0.0;
+        for (int e = 0; e < DMAX; ++e) w[e] = ACT1(e) ? err_weight(P.atol, P.rtol, y[e]) : 0.0;
     };
     auto cold_start = [&](double t0, const double2 (&y0)[DMAX], double h0) {
         t = t0; t_lo = t; q = 1; h = h0;
