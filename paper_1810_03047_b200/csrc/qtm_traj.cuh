@@ -960,6 +960,25 @@ struct HistT {
             H1::rescale(zc, o, q, ratio);
         });
     }
+    // commit, then post(e, z0) with component e's committed row 0 (the error
+    // weights are computed there, while the component is in registers)
+    template <class Post>
+    __device__ __forceinline__ static void commit(Z& z, const O& ovf, int q, const double* l,
+                                                  const double2 (&ev)[E], Post&& post) {
+#define CALL_(Q)                                                                        \
+        per_comp_q<Q>(z, [&](double2 (&zc)[ROWS][1], int e) {                           \
+            const double2 ev1[1] = {sel(ev, e)};                                        \
+            H1::template commit_q<Q>(zc, l, ev1);                                       \
+            post(e, zc[0][0]);                                                          \
+        })
+        QTM_TM_QSWITCH(CALL_)
+#undef CALL_
+        per_comp<true>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
+            const double2 ev1[1] = {sel(ev, e)};
+            H1::commit(zc, o, q, l, ev1);
+            post(e, zc[0][0]);
+        });
+    }
     __device__ __forceinline__ static void commit(Z& z, const O& ovf, int q, const double* l,
                                                   const double2 (&ev)[E]) {
 #define CALL_(Q)                                                                        \
@@ -1496,7 +1515,15 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #pragma unroll
                                 for (int e = 0; e < E; ++e) evr[e] = ACT(e) ? ecurp[II(e)] : make_double2(0.0, 0.0);
                             }
-                            H::commit(z, OVF(), q, P.l[q], evr);
+                            if constexpr (TM) {
+                                // the error weights of the accepted state from each
+                                // committed z0 component inside the TMEM pass
+                                H::commit(z, OVF(), q, P.l[q], evr, [&](int e, double2 z0n) {
+                                    W(e) = ACT(e) ? err_weight(P.atol, P.rtol, z0n) : 0.0;
+                                });
+                            } else {
+                                H::commit(z, OVF(), q, P.l[q], evr);
+                            }
                             break;  // accepted
                         }
                     }
@@ -1536,10 +1563,12 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 ws.t_lo = t;
                 t += h;
                 ws.c_steps++;
+                if constexpr (!TM) {  // (TM: computed in the commit pass)
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const double2 z0 = H::at(z, 0, e);
-                    W(e) = ACT(e) ? err_weight(P.atol, P.rtol, z0) : 0.0;
+                    for (int e = 0; e < E; ++e) {
+                        const double2 z0 = H::at(z, 0, e);
+                        W(e) = ACT(e) ? err_weight(P.atol, P.rtol, z0) : 0.0;
+                    }
                 }
                 PH_MARK(11);  // [11] accepted-step bookkeeping + error weights
                 ialth -= 1;
