@@ -89,6 +89,23 @@ def test_dimension_3000(oracle_lib):
     _check(pk, 8, oracle_lib)
 
 
+@pytest.mark.parametrize("n_fock", [3, 4])
+def test_small_kernel_three_and_four_levels(n_fock, oracle_lib):
+    """d = 3 and 4 run on the one-thread-per-trajectory kernel with d_max = 4
+    (variant 42, automatic for 2 < d <= 4): padded components inactive."""
+    pk = pack_problem(_cavity(n_fock))
+    out = _check(pk, 96, oracle_lib)
+    assert out.variant == 42
+
+
+@pytest.mark.parametrize("n_fock", [600, 777])
+def test_tmem_variant_on_ragged_dimensions(n_fock, oracle_lib):
+    """The TMEM history variant (automatic for 512 < d <= 1024) on states
+    that fill only part of its 1024 components."""
+    out = _check(pack_problem(_cavity(n_fock, t_to=1.0, n_steps=10)), 16, oracle_lib)
+    assert out.variant == 39
+
+
 def test_fp64_pipe_probes():
     """The roofline denominators are measured on the device: DFMA and the
     FP64 tensor pipe (DMMA m8n8k4).  B200's FP64 tensor throughput is no
