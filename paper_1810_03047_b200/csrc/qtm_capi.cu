@@ -767,10 +767,14 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         // BDF: one kernel per block size; the per-trajectory workspace (history,
         // Newton vectors, LU of the iteration matrix) goes to shared memory when
         // it fits, else to a per-CTA slice of HBM
-        // 32 threads for small d (c2 BDF: 2x faster than 128); from d = 65 the
-        // d^2-parallel factorisation / inversion phases want more warps
-        // (c3 BDF: 256 threads +5 % over 128)
-        p->bdf_threads = d->dim <= 64 ? 32 : 256;
+        // 32 threads for small d (c2 BDF: 2x faster than 128).  64 < d <= 256
+        // (the explicit-inverse range): 128 threads with the workspace in
+        // HBM -- L2-resident, 4 trajectories per SM instead of the one a
+        // shared-memory workspace allows (c3 BDF: 3.17k vs 1.92k
+        // trajectories/s; 64 threads x 8 per SM: 2.20k, 256 x 1: 1.59k).
+        // Above d = 256: 256 threads (the blocked LU's tiles).
+        p->bdf_threads = d->dim <= 64 ? 32 : (d->dim <= 256 ? 128 : 256);
+        const bool bdf_hbm_many = d->dim > 64 && d->dim <= 256;
         // Newton solves: substitution with the LU (zgetrs) for small d, where
         // the matrix is refactored every few attempts; the explicit inverse
         // (zgetri) for 48 <= d <= 256, where 2d barrier-separated substitution
@@ -780,12 +784,16 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         if (const char* ev = getenv("QTM_BDF_SOLVE")) p->bdf_inverse = strcmp(ev, "lu") != 0;
         if (const char* ev = getenv("QTM_BDF_THREADS")) {  // A/B experiments
             const int v = atoi(ev);
-            if (v == 32 || v == 256) p->bdf_threads = v;
+            if (v == 32 || v == 64 || v == 128 || v == 256) p->bdf_threads = v;
         }
-        const void* const fn_g = p->bdf_threads == 32 ? (const void*)bdf_kernel<32, false>
-                                                      : (const void*)bdf_kernel<256, false>;
-        const void* const fn_s = p->bdf_threads == 32 ? (const void*)bdf_kernel<32, true>
-                                                      : (const void*)bdf_kernel<256, true>;
+        const void* const fn_g = p->bdf_threads == 32    ? (const void*)bdf_kernel<32, false>
+                                 : p->bdf_threads == 64  ? (const void*)bdf_kernel<64, false>
+                                 : p->bdf_threads == 128 ? (const void*)bdf_kernel<128, false>
+                                                         : (const void*)bdf_kernel<256, false>;
+        const void* const fn_s = p->bdf_threads == 32    ? (const void*)bdf_kernel<32, true>
+                                 : p->bdf_threads == 64  ? (const void*)bdf_kernel<64, true>
+                                 : p->bdf_threads == 128 ? (const void*)bdf_kernel<128, true>
+                                                         : (const void*)bdf_kernel<256, true>;
         p->bdf_fn = fn_g;  // the static shared memory is the same in both
         p->bdf_ws_elems = BdfLayout::make(d->dim).total;
         cudaFuncAttributes battr;
@@ -793,7 +801,9 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         if (cudaFuncGetAttributes(&battr, p->bdf_fn) == cudaSuccess) bstatic = battr.sharedSizeBytes;
         const size_t bcap = (size_t)smem_cap > bstatic ? (size_t)smem_cap - bstatic : 0;
         const size_t bytes = sizeof(double2) * (size_t)p->bdf_ws_elems;
-        p->bdf_in_smem = bytes <= bcap;
+        p->bdf_in_smem = bytes <= bcap && !bdf_hbm_many;
+        if (const char* ev = getenv("QTM_BDF_HBM"))  // A/B: 1 = workspace in HBM/L2, 0 = in smem if it fits
+            p->bdf_in_smem = atoi(ev) == 0 && bytes <= bcap;
         if (p->bdf_in_smem) p->bdf_fn = fn_s;
         // HBM workspace with 256 threads: the blocked LU's tiles in shared memory
         p->smem = p->bdf_in_smem ? bytes : (p->bdf_threads == 256 ? sizeof(double2) * LU_TILE_ELEMS : 0);

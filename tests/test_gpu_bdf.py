@@ -58,8 +58,9 @@ def _cavity(n_fock, kappa=0.5, t_to=10.0, n_steps=100):
                                          options=RunOptions(log_jumps=True))
 
 
-# d = 20 / 80: workspace in shared memory (32 / 128 threads); d = 150, 300:
-# the d^2 LU and the vectors in a per-CTA slice of HBM (128 / 256 threads)
+# d = 20: workspace in shared memory (32 threads); d = 80, 150: the d^2
+# inverse and the vectors in a per-CTA slice of HBM/L2 (128 threads, 4
+# trajectories per SM); d = 300: HBM, 256 threads, blocked LU
 @pytest.mark.parametrize("name,n", [("bdf_c2", 256), ("bdf_c3", 48), ("cav150", 12), ("cav300", 4)])
 def test_bdf_device_matches_oracle(name, n, oracle_lib):
     p = goldens.load(name).problem if name.startswith("bdf_") else \
@@ -69,7 +70,7 @@ def test_bdf_device_matches_oracle(name, n, oracle_lib):
         lay = dp.layout()
         out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
     assert out.rc == 0, out.error
-    assert (lay["smem_rows"] > 0) == (pk.dim <= 80)
+    assert (lay["smem_rows"] > 0) == (pk.dim <= 64)
     ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
     assert ref["rc"] == 0
     _compare(out, ref["values"], ref["jump_count"],
@@ -80,6 +81,22 @@ def test_bdf_device_matches_oracle(name, n, oracle_lib):
         a, b = int(out.stats[:, col].sum()), int(ref["stats"][:, col].sum())
         assert abs(a - b) <= max(2, 0.005 * b), (col, a, b)
     np.testing.assert_allclose(out.sum / n, ref["values"].mean(axis=0), rtol=0, atol=TOL)
+
+
+def test_bdf_shared_memory_workspace_d80(monkeypatch, oracle_lib):
+    """c3 BDF with the whole workspace in shared memory (one 256-thread CTA
+    per SM, the round-1 placement; forced): same trajectories as the oracle."""
+    monkeypatch.setenv("QTM_BDF_HBM", "0")
+    monkeypatch.setenv("QTM_BDF_THREADS", "256")
+    pk = pack_problem(goldens.load("bdf_c3").problem)
+    n = 24
+    with DeviceProblem(pk) as dp:
+        assert dp.layout()["smem_rows"] > 0
+        out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
+    assert out.rc == 0, out.error
+    ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
+    _compare(out, ref["values"], ref["jump_count"],
+             [ref["jump_t"][i] for i in range(n)], [ref["jump_idx"][i] for i in range(n)])
 
 
 def test_bdf_run_gpu_end_to_end(oracle_lib):
