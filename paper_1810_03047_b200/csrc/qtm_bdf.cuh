@@ -39,6 +39,10 @@
 #pragma once
 #include "qtm_traj.cuh"
 
+#ifndef QTM_BDF128_MINB
+#define QTM_BDF128_MINB 4  // 128-thread BDF CTAs per SM (the HBM-workspace range 64 < d <= 256)
+#endif
+
 namespace qtm {
 
 constexpr int BDF_ROWS = 7;  // BDF order <= 6 (ode.py:46): rows 0..6
@@ -605,7 +609,7 @@ __device__ __forceinline__ double2 bdf_horner(const double2* Z, int d, int q, do
 // loads/stores that resolve the address space at run time)
 // (one-warp CTAs: capped at 128 registers so ~16 trajectories share an SM)
 template <int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, NT == 32 ? 16 : (NT == 64 ? 8 : (NT == 128 ? 4 : 1)))
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : (NT == 64 ? 8 : (NT == 128 ? QTM_BDF128_MINB : 1)))
 bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunParams R,
            const __grid_constant__ BdfParams B) {
     constexpr int NW = NT / 32;
