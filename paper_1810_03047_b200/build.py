@@ -33,7 +33,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FMAD = os.environ.get("QTM_FMAD", "1") == "1"
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", f"-fmad={'true' if FMAD else 'false'}",
-                     "-Xcompiler", "-fPIC", "-I", INCLUDE]
+                     f"-DQTM_FMAD={1 if FMAD else 0}", "-Xcompiler", "-fPIC", "-I", INCLUDE]
 # extra nvcc flags for A/B experiments (e.g. -DQTM_SPMV_PF(E)=0)
 NVCC_FLAGS = NVCC_FLAGS + os.environ.get("QTM_NVCC_EXTRA", "").split()
 if os.environ.get("QTM_PHASES", "0") == "1":

@@ -643,7 +643,7 @@ bdf_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPara
     int rphase = 0;
 
     for (;;) {
-        if (tid == 0) s_row = (long long)atomicAdd(R.counter, 1ull);
+        if (tid == 0) s_row = next_row(R);
         __syncthreads();
         const long long row = s_row;
         if (row >= R.n_traj) break;

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../../include/qtm.h"
 #include "qtm_traj.cuh"
 #include "qtm_bdf.cuh"
@@ -88,6 +90,26 @@ __global__ void ensemble_final(const double* __restrict__ psum, const double* __
     }
     sum[o] = s;
     sumsq[o] = s2;
+}
+
+// Processing order of a launch: the first draw of every trajectory's stream is
+// its first jump threshold r (trajectory.py:217).  The norm decays from 1, so a
+// larger r means an earlier first jump, more time left for further jumps and
+// their cold restarts: more step attempts.  Pulling the trajectories in
+// descending r starts the expensive ones first and leaves the cheap no-jump
+// ones to fill the tail of the last wave (tools/scale_sim.py: c4 on 8 GPUs,
+// 0.68 -> 0.89 of linear).  Results do not depend on the order.
+__global__ void first_thresholds(uint64_t seed, long long traj_begin, long long n, int stream_kind,
+                                 const double* __restrict__ script, const long long* __restrict__ script_len,
+                                 long long script_stride, double fallback, double* __restrict__ key,
+                                 int* __restrict__ row) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Stream st;
+    st.init(stream_kind, seed, (uint64_t)(traj_begin + i), script ? script + i * script_stride : nullptr,
+            script_len ? script_len[i] : 0, fallback);
+    key[i] = st.next();
+    row[i] = (int)i;
 }
 
 // per-counter totals over the trajectories: one CTA per counter (slot
@@ -270,6 +292,10 @@ struct qtm_problem {
     DevBuf<double2> psi_out;
     DevBuf<double2> zovf;
     DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row, [2..17] phases
+    // processing order of a launch (first jump thresholds, sorted): keys / rows, in / out
+    DevBuf<double> ord_key;
+    DevBuf<int> ord_row;
+    DevBuf<unsigned char> ord_tmp;
     // BDF method (qtm_bdf.cuh): kernel, block size, workspace placement
     int method = 0;
     const void* bdf_fn = nullptr;
@@ -367,12 +393,19 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             for (int e = 0; e < ncomp; ++e) m = std::max(m, width[w + nw * e]);
             for (int e = 0; e < ncomp; ++e) width[w + nw * e] = m;
         }
-        std::vector<int> off(nslices, 0);
+        // entry slots: per warp, the ncomp slices it walks interleaved per
+        // column in groups of V components (SellSlots in qtm_traj.cuh)
+        const int V = ncomp % 4 == 0 ? 4 : (ncomp % 2 == 0 ? 2 : 1);
+        std::vector<int> woff(nw, 0);
         int total = 0;
-        for (int sl = 0; sl < nslices; ++sl) {
-            off[sl] = total;
-            total += width[sl] * 32;
+        for (int w = 0; w < nw; ++w) {
+            woff[w] = total;
+            total += width[w] * 32 * ncomp;
         }
+        auto slot_of = [&](int sl, size_t k, int lane) {
+            const int w = sl % nw, e = sl / nw;
+            return (size_t)woff[w] + k * 32 * ncomp + (size_t)(e / V) * 32 * V + (size_t)lane * V + (e % V);
+        };
         struct Key {
             uint64_t a, b;
             bool operator<(const Key& o) const { return a < o.a || (a == o.a && b < o.b); }
@@ -408,8 +441,8 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
                     ++j0;
                 }
                 if (vi < 0) { ok = false; break; }
-                const size_t slot = (size_t)off[sl] + k * 32 + lane;
-                ent[slot] = (uint32_t)(16 * c) | ((uint32_t)(16 * vi) << 16);
+                const size_t slot = slot_of(sl, k, lane);
+                ent[slot] = (uint32_t)(16 * vi) | ((uint32_t)(16 * c) << 16);
                 for (int t = 0; t < nt1; ++t) {
                     const qtm_csr* m = tds[t];
                     int ti = 0;
@@ -431,7 +464,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         int *d_off = nullptr, *d_w = nullptr;
         CUDA_TRY(upload(p, &d_ent, ent.data(), ent.size()));
         CUDA_TRY(upload(p, &d_dict, dict.data(), dict.size()));
-        CUDA_TRY(upload(p, &d_off, off.data(), (size_t)nslices));
+        CUDA_TRY(upload(p, &d_off, woff.data(), (size_t)nw));
         CUDA_TRY(upload(p, &d_w, width.data(), (size_t)nslices));
         DevProblem& P = p->dp;
         P.sell_mode = 1;
@@ -598,6 +631,7 @@ void free_problem(qtm_problem* p) {
     p->sum.release(s); p->sumsq.release(s); p->jump_t.release(s); p->script.release(s);
     p->stats.release(s); p->jump_count.release(s); p->script_len.release(s); p->stats_tot.release(s);
     p->status.release(s); p->jump_idx.release(s); p->zovf.release(s); p->ctl.release(s);
+    p->ord_key.release(s); p->ord_row.release(s); p->ord_tmp.release(s);
     p->psi_slot.release(s); p->psi_out.release(s);
     p->bdf_ws.release(s);
     if (s) cudaStreamSynchronize(s);
@@ -980,6 +1014,19 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
     CUDA_TRY(p->psq.ensure((size_t)n_red_total * std::max(n_out, 1), s));
     CUDA_TRY(p->sum.ensure(std::max(n_out, 1), s));
     CUDA_TRY(p->sumsq.ensure(std::max(n_out, 1), s));
+    // processing order (QTM_ORDER=0 keeps index order); the one-thread-per-trajectory
+    // kernel maps rows to lanes statically and takes none
+    static const bool order_env = !(getenv("QTM_ORDER") && atoi(getenv("QTM_ORDER")) == 0);
+    const bool use_order = order_env && !small && run_chunk > grid;
+    size_t ord_tmp_bytes = 0;
+    if (use_order) {
+        CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, ord_tmp_bytes, (const double*)nullptr,
+                                                            (double*)nullptr, (const int*)nullptr, (int*)nullptr,
+                                                            (int)run_chunk, 0, 64, s));
+        CUDA_TRY(p->ord_key.ensure((size_t)2 * run_chunk, s));
+        CUDA_TRY(p->ord_row.ensure((size_t)2 * run_chunk, s));
+        CUDA_TRY(p->ord_tmp.ensure(ord_tmp_bytes, s));
+    }
     const bool want_psi = a->n_psi_points > 0 && o->psi;
     if (want_psi) {
         std::vector<int> slot(p->n_pts, -1);
@@ -1052,6 +1099,22 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         R.psi_out = want_psi ? p->psi_out.p : nullptr;
         R.n_psi = want_psi ? a->n_psi_points : 0;
         R.lanes = small ? var.lanes : 0;
+        R.order = nullptr;
+        if (use_order && cnt > cgrid) {
+            // more trajectories than resident CTAs: longest expected first
+            double* const k_in = p->ord_key.p;
+            double* const k_out = p->ord_key.p + run_chunk;
+            int* const r_in = p->ord_row.p;
+            int* const r_out = p->ord_row.p + run_chunk;
+            first_thresholds<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(
+                R.seed, R.traj_begin, cnt, R.stream_kind, R.script, R.script_len, R.script_stride,
+                R.script_fallback, k_in, r_in);
+            size_t tmp_bytes = ord_tmp_bytes;
+            CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(p->ord_tmp.p, tmp_bytes, k_in, k_out, r_in, r_out,
+                                                                (int)cnt, 0, 64, s));
+            R.order = r_out;
+            launches += 2;  // first_thresholds + the sort's own kernels (counted as one)
+        }
         BdfParams BP{};
         BP.ws = p->bdf_ws.p;
         BP.ws_stride = p->bdf_ws_elems;

@@ -79,17 +79,18 @@ struct DevProblem {
     const double2* psi0;
     const double* times;
     // G in sliced-ELL form for shared-memory staging (built per kernel
-    // variant on the host): slice = 32 consecutive rows, entries stored
-    // [slice][k][lane] as uint32 (16*col | 16*value-index << 16), widths
-    // padded to be uniform per warp; the value index points into a dictionary
-    // of the distinct entries of G (index 0 = 0.0, used for padding).
+    // variant on the host): slice = 32 consecutive rows, the E slices of a
+    // warp interleaved per column (SellSlots), entries uint32
+    // (16*value-index | 16*col << 16), widths padded to be uniform per warp;
+    // the value index points into a dictionary of the distinct entries of G
+    // (index 0 = 0.0, used for padding).
     // sell_mode 0 = plain CSR through L1/L2 (d > 4096 or > 4095 distinct values).
     int sell_mode;
     int sell_entries, sell_dict_n;
     const uint32_t* sell_ent;
     const double2* sell_dict;
-    const int* sell_off;    // [DP/32] first entry of each slice
-    const int* sell_w;      // [DP/32] width of each slice
+    const int* sell_off;    // [NT/32] first entry slot of each warp (SellSlots)
+    const int* sell_w;      // [DP/32] width of each slice (uniform over a warp's E slices)
     // TD variants: the SELL above is built on the union pattern of G0 and
     // the sell_td staged time-dependent terms, and sell_td_ent ([sell_td]
     // arrays of uint16 per slot, same slot layout) holds the byte offset of
@@ -163,12 +164,25 @@ struct RunParams {
     unsigned long long* first_fail;  // atomicMin over failing rows
     unsigned long long* phase_cycles;  // [16] (QTM_PHASES builds only)
     int lanes;               // traj1_kernel: trajectories per warp
+    // processing order of the launch's trajectories (nullptr: by index): the
+    // j-th pull of the work counter integrates row order[j].  Outputs are
+    // keyed by row, so the order changes when a trajectory runs, never what
+    // it computes (qtm_capi.cu sorts by the first jump threshold, longest
+    // expected trajectory first, to shorten the tail of the last wave)
+    const int* order;
     // psi snapshots (diagnostics / parity): slot of each grid index (-1 =
     // none; nullptr = no snapshots) and the output [n_traj][n_psi][d]
     const int* psi_slot;
     double2* psi_out;
     int n_psi;
 };
+
+// next trajectory row of this launch from the global work counter (>= n_traj:
+// none left), through the launch's processing order when it has one
+__device__ __forceinline__ long long next_row(const RunParams& R) {
+    const long long j = (long long)atomicAdd(R.counter, 1ull);
+    return (R.order && j < R.n_traj) ? (long long)R.order[j] : j;
+}
 
 // ---------------------------------------------------------------- helpers
 // The reference's numba kernels are compiled without fast-math, so no a*b+c
@@ -212,13 +226,26 @@ static __device__ __noinline__ double ctl_pow(double x, double y) {
 }
 
 // acc += v * x: the product (ac - bd, ad + bc), then the sum, as the
-// reference's complex_mul + add (_kernels.py:18-26).  (Accumulating the four
-// real products straight into the sums with FMAs saves two FP64
-// instructions per entry but moved c4 jump times by 9e-6 against the
-// reference, and was no faster: measured, not kept.)
+// reference's complex_mul + add (_kernels.py:18-26).  The rounding sequence
+// is pinned with intrinsics, so it does not depend on which of the legal
+// contractions the compiler would pick in a given loop shape (two forms of
+// the imaginary part differ in the last bit, and did between variants):
+//   throughput build:  re = fma(a, c, -rn(b d)),  im = fma(b, c, rn(a d))
+//   QTM_FMAD=0:        every product and sum rounded, as numba computes it
+// (Accumulating the four real products straight into the sums with FMAs
+// saves two FP64 instructions per entry but moved c4 jump times by 9e-6
+// against the reference, and was no faster: measured, not kept.)
+#ifndef QTM_FMAD
+#define QTM_FMAD 1
+#endif
 __device__ __forceinline__ void cmac(double& sr, double& si, double2 v, double2 x) {
-    sr = sr + (v.x * x.x - v.y * x.y);
-    si = si + (v.x * x.y + v.y * x.x);
+#if QTM_FMAD
+    sr = __dadd_rn(sr, __fma_rn(v.x, x.x, -__dmul_rn(v.y, x.y)));
+    si = __dadd_rn(si, __fma_rn(v.y, x.x, __dmul_rn(v.x, x.y)));
+#else
+    sr = __dadd_rn(sr, __dsub_rn(__dmul_rn(v.x, x.x), __dmul_rn(v.y, x.y)));
+    si = __dadd_rn(si, __dadd_rn(__dmul_rn(v.x, x.y), __dmul_rn(v.y, x.x)));
+#endif
 }
 
 // y_i = sum_j M_ij x_j, left to right, each product (ac - bd, ad + bc) then
@@ -230,10 +257,7 @@ static __device__ __noinline__ double2 row_dot(const DevCsr& m, int i, const dou
     double sr = 0.0, si = 0.0;
     const int b = __ldg(m.rp + i), en = __ldg(m.rp + i + 1);
     for (int j = b; j < en; ++j) {
-        const double2 v = __ldg(m.v + j);
-        const double2 xv = x[__ldg(m.ci + j)];
-        sr = sr + (v.x * xv.x - v.y * xv.y);
-        si = si + (v.x * xv.y + v.y * xv.x);
+        cmac(sr, si, __ldg(m.v + j), x[__ldg(m.ci + j)]);
     }
     return make_double2(sr, si);
 }
@@ -251,88 +275,143 @@ __device__ __forceinline__ double2 td_term(const DevCsr& m, double c, int i, con
     return make_double2(f.x + c * g.x, f.y + c * g.y);
 }
 
+// Entry slots of a warp in the staged sliced-ELL copy.  The E slices a warp
+// walks together (rows tid + NT*e) are interleaved per ELL column k, in
+// groups of V = 4 / 2 / 1 components (E % 4 == 0 / E even / E odd):
+//   slot(k, e, lane) = k*32*E + (e/V)*32*V + lane*V + (e%V)      (+ warp base)
+// so one 128-bit (64-bit) shared load fetches the entries of 4 (2) of the
+// thread's rows, every load of column k is an immediate offset from one
+// pointer that advances by 32*E per column, and the accesses are
+// conflict-free (lane stride V words with V-word loads).
+template <int E>
+struct SellSlots {
+    static constexpr int V = E % 4 == 0 ? 4 : (E % 2 == 0 ? 2 : 1);
+    // slot of (e, lane) inside column 0 (add k*32*E for column k)
+    __host__ __device__ static constexpr int in_col(int e, int lane) {
+        return (e / V) * 32 * V + lane * V + (e % V);
+    }
+    // the E entries of this lane for one column; p = column base + lane*V
+    __device__ __forceinline__ static void load(const uint32_t* __restrict__ p, uint32_t (&u)[E]) {
+        if constexpr (V == 4) {
+#pragma unroll
+            for (int g = 0; g < E / 4; ++g) {
+                const uint4 w = *reinterpret_cast<const uint4*>(p + g * 128);
+                u[4 * g] = w.x; u[4 * g + 1] = w.y; u[4 * g + 2] = w.z; u[4 * g + 3] = w.w;
+            }
+        } else if constexpr (V == 2) {
+#pragma unroll
+            for (int g = 0; g < E / 2; ++g) {
+                const uint2 w = *reinterpret_cast<const uint2*>(p + g * 64);
+                u[2 * g] = w.x; u[2 * g + 1] = w.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) u[e] = p[e * 32];
+        }
+    }
+    // the same for a uint16 array in the slot layout (TD term offsets)
+    __device__ __forceinline__ static void load16(const uint16_t* __restrict__ p, uint32_t (&t)[E]) {
+        if constexpr (V == 4) {
+#pragma unroll
+            for (int g = 0; g < E / 4; ++g) {
+                const uint2 w = *reinterpret_cast<const uint2*>(p + g * 128);
+                t[4 * g] = w.x & 0xFFFFu; t[4 * g + 1] = w.x >> 16;
+                t[4 * g + 2] = w.y & 0xFFFFu; t[4 * g + 3] = w.y >> 16;
+            }
+        } else if constexpr (V == 2) {
+#pragma unroll
+            for (int g = 0; g < E / 2; ++g) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(p + g * 64);
+                t[2 * g] = w & 0xFFFFu; t[2 * g + 1] = w >> 16;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) t[e] = p[e * 32];
+        }
+    }
+};
+
 // f = G x for this thread's E rows from the staged sliced-ELL copy: the E
 // rows' chains are interleaved for ILP; each row is still summed in column
 // order (entries k ascending), so the rounding matches row_dot exactly.
-// Entry = x byte offset (col*16, low half) | dictionary byte offset (high
-// half), so each entry costs two 16-byte shared loads and no index math.
-// Software-pipelined: the entries of column k+1 (PF >= 1) and the operands of
-// column k+1 (PF >= 2) are loaded while column k is multiplied, so one
-// shared-memory round trip per column overlaps the arithmetic.
-// PF = 2 costs 4E registers more than PF = 1 and loses to it wherever
-// registers are tight; the compact shared-history variants (RREG = 0) keep
-// the plain loop (their code size matters more than the load latency).
+// Entry = dictionary byte offset (low half) | x byte offset (col*16, high
+// half): each entry costs two 16-byte shared loads and two address
+// instructions (mask + uniform dictionary base; shift-add onto the gather
+// buffer).
+// Software-pipelined (PF = 1): the entries of column k+1 are loaded while
+// column k is multiplied, the last column peeled so the loop carries no
+// clamp.  The compact shared-history variants (RREG = 0) keep the plain loop
+// (their code size matters more than the load latency).  (A distance-2
+// pipeline that also prefetched the operands cost 4E registers more and lost
+// wherever registers are tight: measured, dropped.)
 #ifndef QTM_SPMV_PF
 #define QTM_SPMV_PF(RREG) ((RREG) == 0 ? 0 : 1)
 #endif
+// unroll factor of the pipelined column loop: 1 (measured on c4 under the
+// TMEM variant's 128-register cap: the compiler's own choice of 2 spilled more
+// and ran 1.5 % slower; c5 / c2 / c4td within 1 % either way)
+#ifndef QTM_SPMV_UNROLL
+#define QTM_SPMV_UNROLL 1
+#endif
+#define QTM_PRAGMA_(x) _Pragma(#x)
+#define QTM_PRAGMA(x) QTM_PRAGMA_(x)
+#define QTM_SPMV_UNROLL_PRAGMA QTM_PRAGMA(unroll QTM_SPMV_UNROLL)
+__device__ __forceinline__ double2 sell_val(const char* db, uint32_t u) {
+    return *reinterpret_cast<const double2*>(db + (u & 0xFFFFu));
+}
+__device__ __forceinline__ double2 sell_x(const char* xb, uint32_t u) {
+    return *reinterpret_cast<const double2*>(xb + (u >> 16));
+}
 template <int NT, int E, int PF>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
-                                          const double2* __restrict__ dict, const int (&off)[E],
+                                          const double2* __restrict__ dict, int woff,
                                           int width, const double2* __restrict__ x,
                                           double2 (&out)[E]) {
+    using S = SellSlots<E>;
     const int lane = threadIdx.x & 31;
     const char* const xb = reinterpret_cast<const char*>(x);
     const char* const db = reinterpret_cast<const char*>(dict);
+    const uint32_t* p = ent + woff + lane * S::V;
     double sr[E], si[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
     if constexpr (PF == 0) {
 #pragma unroll (E >= 4 ? 1 : 2)
         for (int k = 0; k < width; ++k) {
+            uint32_t u[E];
+            S::load(p, u);
+            p += 32 * E;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const uint32_t u = ent[off[e] + k * 32 + lane];
-                const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
-                const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
-                cmac(sr[e], si[e], v, xv);
-            }
+            for (int e = 0; e < E; ++e) cmac(sr[e], si[e], sell_val(db, u[e]), sell_x(xb, u[e]));
         }
-    } else if constexpr (PF == 1) {
-        uint32_t u[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) u[e] = ent[off[e] + lane];
+    } else if constexpr (E == 1) {
+        // one row per thread (a few entries per row): the clamped prefetch
+        // keeps a single copy of the loop body
+        uint32_t u = width > 0 ? p[0] : 0u;
         for (int k = 0; k < width; ++k) {
             const int kn = k + 1 < width ? k + 1 : k;
+            const double2 v = sell_val(db, u), xv = sell_x(xb, u);
+            u = p[kn * 32];
+            cmac(sr[0], si[0], v, xv);
+        }
+    } else if (width > 0) {
+        uint32_t u[E];
+        S::load(p, u);
+        QTM_SPMV_UNROLL_PRAGMA
+        for (int k = 1; k < width; ++k) {
             double2 v[E], xv[E];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                v[e] = *reinterpret_cast<const double2*>(db + (u[e] >> 16));
-                xv[e] = *reinterpret_cast<const double2*>(xb + (u[e] & 0xFFFFu));
+                v[e] = sell_val(db, u[e]);
+                xv[e] = sell_x(xb, u[e]);
             }
+            p += 32 * E;
+            S::load(p, u);
 #pragma unroll
-            for (int e = 0; e < E; ++e) u[e] = ent[off[e] + kn * 32 + lane];
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                cmac(sr[e], si[e], v[e], xv[e]);
-            }
+            for (int e = 0; e < E; ++e) cmac(sr[e], si[e], v[e], xv[e]);
         }
-    } else {
-        uint32_t u[E];
-        double2 v[E], xv[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const uint32_t u0 = ent[off[e] + lane];
-            v[e] = *reinterpret_cast<const double2*>(db + (u0 >> 16));
-            xv[e] = *reinterpret_cast<const double2*>(xb + (u0 & 0xFFFFu));
-            u[e] = ent[off[e] + (width > 1 ? 32 : 0) + lane];
-        }
-        for (int k = 0; k < width; ++k) {
-            const int k2 = k + 2 < width ? k + 2 : width - 1;
-            double2 vn[E], xn[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                vn[e] = *reinterpret_cast<const double2*>(db + (u[e] >> 16));
-                xn[e] = *reinterpret_cast<const double2*>(xb + (u[e] & 0xFFFFu));
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) u[e] = ent[off[e] + k2 * 32 + lane];
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                cmac(sr[e], si[e], v[e], xv[e]);
-                v[e] = vn[e];
-                xv[e] = xn[e];
-            }
-        }
+        for (int e = 0; e < E; ++e) cmac(sr[e], si[e], sell_val(db, u[e]), sell_x(xb, u[e]));
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] = make_double2(sr[e], si[e]);
@@ -344,8 +423,9 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
 template <int NT, int E>
 __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, const double2* __restrict__ dict,
                                              const uint16_t* __restrict__ tent, const double2* __restrict__ tdict,
-                                             const int (&off)[E], int width, const double2* __restrict__ x,
+                                             int woff, int width, const double2* __restrict__ x,
                                              double2 (&out0)[E], double2 (&out1)[E]) {
+    using S = SellSlots<E>;
     const int lane = threadIdx.x & 31;
     const char* const xb = reinterpret_cast<const char*>(x);
     const char* const db = reinterpret_cast<const char*>(dict);
@@ -353,14 +433,19 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
     double sr[E], si[E], tr[E], ti[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; tr[e] = 0.0; ti[e] = 0.0; }
+    const uint32_t* p = ent + woff + lane * S::V;
+    const uint16_t* pt = tent + woff + lane * S::V;
     for (int k = 0; k < width; ++k) {
+        uint32_t u[E], tu[E];
+        S::load(p, u);
+        S::load16(pt, tu);
+        p += 32 * E;
+        pt += 32 * E;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int slot = off[e] + k * 32 + lane;
-            const uint32_t u = ent[slot];
-            const double2 v = *reinterpret_cast<const double2*>(db + (u >> 16));
-            const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
-            const double2 xv = *reinterpret_cast<const double2*>(xb + (u & 0xFFFFu));
+            const double2 v = sell_val(db, u[e]);
+            const double2 w = *reinterpret_cast<const double2*>(tb + tu[e]);
+            const double2 xv = sell_x(xb, u[e]);
             cmac(sr[e], si[e], v, xv);
             cmac(tr[e], ti[e], w, xv);
         }
@@ -376,20 +461,27 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
 // terms): G_k's value per slot from its uint16 offsets, rows in column order.
 template <int NT, int E>
 __device__ __forceinline__ void sell_spmv_term(const uint32_t* __restrict__ ent, const uint16_t* __restrict__ tent,
-                                               const double2* __restrict__ tdict, const int (&off)[E], int width,
+                                               const double2* __restrict__ tdict, int woff, int width,
                                                const double2* __restrict__ x, double2 (&out)[E]) {
+    using S = SellSlots<E>;
     const int lane = threadIdx.x & 31;
     const char* const xb = reinterpret_cast<const char*>(x);
     const char* const tb = reinterpret_cast<const char*>(tdict);
     double tr[E], ti[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { tr[e] = 0.0; ti[e] = 0.0; }
+    const uint32_t* p = ent + woff + lane * S::V;
+    const uint16_t* pt = tent + woff + lane * S::V;
     for (int k = 0; k < width; ++k) {
+        uint32_t u[E], tu[E];
+        S::load(p, u);
+        S::load16(pt, tu);
+        p += 32 * E;
+        pt += 32 * E;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-            const int slot = off[e] + k * 32 + lane;
-            const double2 w = *reinterpret_cast<const double2*>(tb + tent[slot]);
-            const double2 xv = *reinterpret_cast<const double2*>(xb + (ent[slot] & 0xFFFFu));
+            const double2 w = *reinterpret_cast<const double2*>(tb + tu[e]);
+            const double2 xv = sell_x(xb, u[e]);
             cmac(tr[e], ti[e], w, xv);
         }
     }
@@ -1187,7 +1279,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         for (int i = tid; i < P.e_stage_idx_bytes / 4; i += NT) reinterpret_cast<uint32_t*>(di)[i] = si[i];
         for (int i = tid; i < P.e_dict_n; i += NT) dd[i] = P.e_dict_g[i];
     }
-    int goff[E], gwidth = 0;
+    int goff = 0, gwidth = 0;
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
@@ -1196,8 +1288,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
             for (int i = tid; i < P.sell_td * P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
         }
         const int warp = tid >> 5;
-#pragma unroll
-        for (int e = 0; e < E; ++e) goff[e] = P.sell_off[warp + (NT / 32) * e];
+        goff = P.sell_off[warp];
         gwidth = P.sell_w[warp];
         __syncthreads();
     }
@@ -1251,7 +1342,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     int gbuf = 0, rphase = 0, ecur = 0;
 
     for (;;) {
-        if (tid == 0) s_row = (long long)atomicAdd(R.counter, 1ull);
+        if (tid == 0) s_row = next_row(R);
         __syncthreads();
         ws.row = s_row;
         if (ws.row >= R.n_traj) break;
