@@ -20,11 +20,23 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/qtm.h"
 #include "qtm_traj.cuh"
 #include "qtm_bdf.cuh"
 #include "qtm_small.cuh"
+
+// NVTX ranges around the host-side phases of the C ABI (problem upload, a run,
+// each chunk's trajectory launch and its reductions): visible in Nsight
+// Systems / ncu --nvtx timelines, free when no tool is attached (NVTX v3 is
+// header-only and resolves its injection library lazily).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace qtm;
 
@@ -687,6 +699,7 @@ int qtm_device_count(void) {
 }
 
 int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
+    NvtxRange nvtx_range("qtm_problem_create");
     if (!d || !out) return set_error(QTM_ERR_ARGS, "null descriptor or output handle");
     *out = nullptr;
     if (d->abi_version != QTM_ABI_VERSION) return set_error(QTM_ERR_ARGS, "ABI version mismatch");
@@ -938,6 +951,7 @@ int qtm_problem_layout(qtm_problem* p, int32_t* reg_rows, int32_t* smem_rows, in
 constexpr long long kRunChunkMax = 1ll << 16;  // trajectories per launch chunk
 
 static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool copy_per_traj) {
+    NvtxRange nvtx_range(copy_per_traj ? "qtm_run" : "qtm_run_resident");
     if (!p || !a || !o) return set_error(QTM_ERR_ARGS, "null argument");
     if (a->traj_end < a->traj_begin || a->traj_begin < 0) return set_error(QTM_ERR_ARGS, "bad trajectory range");
     if (!o->sum) return set_error(QTM_ERR_ARGS, "out->sum is required");
@@ -1121,10 +1135,13 @@ static int run_impl(qtm_problem* p, const qtm_run_args* a, qtm_run_out* o, bool 
         BP.in_smem = p->bdf_in_smem ? 1 : 0;
         BP.inverse = p->bdf_inverse ? 1 : 0;
         void* kargs[] = {(void*)&p->dp, (void*)&R, (void*)&BP};
+        nvtxRangePushA(bdf ? "bdf_kernel chunk" : small ? "traj1_kernel chunk" : "traj_kernel chunk");
         CUDA_TRY(cudaEventRecord(p->ev[1], s));
         CUDA_TRY(cudaLaunchKernel(kfn, dim3((unsigned)cgrid), dim3(kthreads), kargs, p->smem, s));
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(p->ev[2], s));
+        nvtxRangePop();
+        NvtxRange nvtx_red("finalize + ensemble reductions");
         const long long cells = cnt * p->n_pts;
         finalize_records<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(
             p->rec_partial.p, p->status.p, p->values.p, cnt, (int)p->n_pts, p->n_expect, nw, p->ctl.p + 1);

@@ -809,6 +809,9 @@ struct Hist {
         for (int jj = 0; jj < RREG; ++jj) if (jj == j) z[jj][e] = v;
     }
 
+    __device__ __forceinline__ static void horner_fast(const Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
+        horner(z, ovf, q, s, out);
+    }
     // psi(s) = Horner over rows q..0 (nordsieck_eval, _kernels.py:61-69)
     __device__ __forceinline__ static void horner(const Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
 #pragma unroll
@@ -890,6 +893,9 @@ struct HistS {
     __device__ __forceinline__ static void set_row_all(Z& z, const O& o, int j, const double2 (&v)[E]) {
 #pragma unroll
         for (int e = 0; e < E; ++e) at(z, j, e) = v[e];
+    }
+    __device__ __forceinline__ static void horner_fast(const Z& z, const O& o, int q, double s, double2 (&out)[E]) {
+        horner(z, o, q, s, out);
     }
     __device__ __forceinline__ static void horner(const Z& z, const O&, int q, double s, double2 (&out)[E]) {
 #pragma unroll
@@ -990,7 +996,7 @@ struct HistT {
     // Order-specialised form for Q <= 7 (every row on chip): only the TMEM
     // rows 2..Q move, in one load of 4(Q-1) columns per component, and the
     // arithmetic is Hist<8, 1>'s straight-line code for order Q.
-    template <int Q, class F>
+    template <int Q, bool STORE = true, class F>
     __device__ __forceinline__ static void per_comp_q(Z& z, F&& f) {
         constexpr int N = Q - 1;  // TMEM rows 2..Q
         if constexpr (N > 0) tm::wait_st();
@@ -1009,6 +1015,7 @@ struct HistT {
             zc[0][0] = z.z0[(DP / E) * e];
             zc[1][0] = z.r1[e];
             f(zc, e);
+            if constexpr (!STORE) continue;
             z.z0[(DP / E) * e] = zc[0][0];
             z.r1[e] = zc[1][0];
             if constexpr (N > 0) {
@@ -1084,6 +1091,19 @@ struct HistT {
             const double2 ev1[1] = {sel(ev, e)};
             H1::commit(zc, o, q, l, ev1);
         });
+    }
+    // the per-step grid recording's Horner (the one hot call site): with every
+    // row on chip (q <= 7) only rows 2..q are loaded, straight-line code
+    __device__ __forceinline__ static void horner_fast(Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
+#define CALL_(Q)                                                                        \
+        per_comp_q<Q, false>(z, [&](double2 (&zc)[ROWS][1], int e) {                    \
+            double2 o1[1];                                                              \
+            H1::template horner_q<Q>(zc, s, o1);                                        \
+            out[e] = o1[0];                                                             \
+        })
+        QTM_TM_QSWITCH(CALL_)
+#undef CALL_
+        horner(z, ovf, q, s, out);
     }
     __device__ __forceinline__ static void horner(Z& z, const O& ovf, int q, double s, double2 (&out)[E]) {
         per_comp<false>(z, ovf, [&](double2 (&zc)[ROWS][1], const typename H1::O& o, int e) {
@@ -1845,7 +1865,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
                 PH_MARK(9);  // [9] jump test (+ jumps)
                 while (ws.t_next <= t) {
                     double2 pg[E];
-                    HORNER((ws.t_next - t) / h, pg);
+                    H::horner_fast(z, OVF(), q, (ws.t_next - t) / h, pg);
                     RECORD(pg, ws.gi);
                     ws.gi++;
                     ws.t_next = ws.gi < npts ? P.times[ws.gi] : CUDART_INF;

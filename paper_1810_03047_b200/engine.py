@@ -137,6 +137,18 @@ def bytes_model(stats_total: dict, packed: PackedProblem) -> float:
     return float(16 * d * (2 * (stats_total["sum_q"] + att) + 2 * att))
 
 
+def smem_model(stats_total: dict, packed: PackedProblem) -> float:
+    """Shared-memory bytes the Adams trajectory kernel moves by construction
+    (DESIGN.md §3): per corrector iteration the staged-operator SpMV reads an
+    entry word, a 16-byte dictionary value and a 16-byte gathered x per
+    nonzero (36 nnz), and the update reads the iterate and the weight and
+    writes the next iterate (40 d); per attempt the predicted z0 is published
+    once (16 d).  Reductions, row 0 of the TMEM variant and recording come on
+    top, so the measured wavefronts (ncu) are higher."""
+    d, nnz = packed.dim, packed.g.nnz
+    return float(stats_total["corr_iters"] * (36 * nnz + 40 * d) + stats_total["attempts"] * 16 * d)
+
+
 @dataclass
 class RunOutput:
     sum: np.ndarray
