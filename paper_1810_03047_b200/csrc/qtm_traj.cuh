@@ -996,17 +996,40 @@ struct HistT {
     // Order-specialised form for Q <= 7 (every row on chip): only the TMEM
     // rows 2..Q move, in one load of 4(Q-1) columns per component, and the
     // arithmetic is Hist<8, 1>'s straight-line code for order Q.
+    // QTM_TM_DB=1: the rows of component e+1 are loaded while
+    // component e is processed (two raw buffers, 4(Q-1) registers more), so
+    // only the first component's TMEM latency is exposed.  Measured on c4:
+    // 111.9 vs 109.2 ms per step -- the second CTA on the SM already hides
+    // that latency, and the extra registers cost more: off by default.
+#ifndef QTM_TM_DB
+#define QTM_TM_DB 0
+#endif
     template <int Q, bool STORE = true, class F>
     __device__ __forceinline__ static void per_comp_q(Z& z, F&& f) {
         constexpr int N = Q - 1;  // TMEM rows 2..Q
+        constexpr int W = 4 * (N > 0 ? N : 1);
         if constexpr (N > 0) tm::wait_st();
+#if QTM_TM_DB
+        uint32_t rawa[W], rawb[W];
+        if constexpr (N > 0) tm::issue_ld(rows_col(z, 0), rawa);
+#endif
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             double2 zc[ROWS][1];
-            uint32_t raw[4 * (N > 0 ? N : 1)];
+#if QTM_TM_DB
+            uint32_t (&raw)[W] = (e & 1) ? rawb : rawa;
+            uint32_t (&nxt)[W] = (e & 1) ? rawa : rawb;
+#else
+            uint32_t raw[W];
+#endif
             if constexpr (N > 0) {
+#if QTM_TM_DB
+                tm::wait_ld(raw);
+                if (e + 1 < E) tm::issue_ld(rows_col(z, e + 1), nxt);
+#else
                 tm::issue_ld(rows_col(z, e), raw);
                 tm::wait_ld(raw);
+#endif
                 double2 t[N > 0 ? N : 1];
                 tm::unpack<(N > 0 ? N : 1)>(raw, t);
 #pragma unroll
