@@ -2,7 +2,7 @@
 # A/B of a tagged library against libqtm.so: bitwise comparison of the
 # per-trajectory outputs on several configs / variants, then bench lines,
 # then (optionally) the GPU suite under the tagged library.
-# usage: gpu_pk.sh TAG LIBTAG [suite]
+# usage: gpu_libcmp.sh TAG LIBTAG [suite]   (libqtm_LIBTAG.so against libqtm.so)
 cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
 TAG=$1; LT=$2
 P=$PWD/paper_1810_03047_b200
