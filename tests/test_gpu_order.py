@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TOOL = os.path.join(HERE, "tools", "lib_dump.py")
 
 # more trajectories than resident CTAs, so the order is in effect
-SPECS = ["c4:700:39", "c3:3000:12", "c2:4800:17", "c5:640:27", "c2+bdf:4000"]
+SPECS = ["c4:700:39", "c3:3000:12", "c2:4800:17", "c5:640:27", "c2+bdf:4000", "c4:600:39:lfsr113"]
 
 
 @pytest.mark.gpu

@@ -2,7 +2,8 @@
 compare two dumps bit for bit (a refactoring that keeps the arithmetic must
 keep every bit: series, jump logs, counters, status).
 
-    QTM_LIB=... python tools/lib_dump.py dump OUT.npz c4:512:39 c5:128:27 ...
+    QTM_LIB=... python tools/lib_dump.py dump OUT.npz c4:512:39 c5:128:27 c2:4000:-1:lfsr113 ...
+    (spec = config[+bdf]:trajectories[:variant[:stream]])
     python tools/lib_dump.py cmp A.npz B.npz
 """
 import os, sys
@@ -17,7 +18,10 @@ def dump(out_path, specs):
     from paper_1810_03047_b200.packing import pack_problem
     arrs = {}
     for spec in specs:
-        name, n, v = (spec.split(":") + ["-1"])[:3]
+        parts = spec.split(":")
+        name, n = parts[0], parts[1]
+        v = parts[2] if len(parts) > 2 else "-1"
+        stream = parts[3] if len(parts) > 3 else "philox"
         method = None
         if name.endswith("+bdf"):
             name, method = name[:-4], "bdf"
@@ -27,7 +31,7 @@ def dump(out_path, specs):
             kw["ode"] = OdeConfig(rtol=1e-8, atol=1e-10, method="bdf")
         pk = pack_problem(configs.build(name, **kw))
         with DeviceProblem(pk, variant=int(v)) as dp:
-            out = run_logged(dp, 987654321, 0, int(n))
+            out = run_logged(dp, 987654321, 0, int(n), stream=stream)
         key = spec.replace(":", "_").replace("+", "_")
         arrs[key + "_values"] = out.values
         arrs[key + "_stats"] = out.stats

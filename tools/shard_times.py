@@ -20,6 +20,7 @@ variant = int(sys.argv[2]) if len(sys.argv) > 2 else -1
 n_total = int(sys.argv[3]) if len(sys.argv) > 3 else N_TRAJECTORIES[name]
 pk = pack_problem(configs.build(name))
 SEED = 987654321
+REPS = int(os.environ.get("SHARD_REPS", "2"))
 rows = []
 with DeviceProblem(pk, variant=variant) as dp:
     dp.run(1, 0, 64, resident=True)
@@ -28,7 +29,7 @@ with DeviceProblem(pk, variant=variant) as dp:
         shards = []
         for rank in range(world):
             b, e = shard_range(n_total, world, rank)
-            ms = min(dp.run(SEED, b, e, resident=True).total_ms for _ in range(2)) if e > b else 0.0
+            ms = min(dp.run(SEED, b, e, resident=True).total_ms for _ in range(REPS)) if e > b else 0.0
             shards.append({"rank": rank, "begin": b, "end": e, "ms": round(ms, 3)})
         t = max(s["ms"] for s in shards)
         t1 = t1 or t
