@@ -304,6 +304,7 @@ struct qtm_problem {
     DevBuf<double2> psi_out;
     DevBuf<double2> zovf;
     DevBuf<unsigned long long> ctl;  // [0] work counter, [1] first failing row, [2..17] phases
+    cudaTextureObject_t sell_tex = 0;  // QTM_SELL_TEX: the value dictionary as a texture
     // processing order of a launch (first jump thresholds, sorted): keys / rows, in / out
     DevBuf<double> ord_key;
     DevBuf<int> ord_row;
@@ -377,7 +378,8 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
 // (sell_td_*); if that does not fit, G0 alone is staged and the G_k stay in
 // L2 (row_dot).
 int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
-               size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {}) {
+               size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {},
+               bool use_tex = false) {
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
@@ -454,7 +456,8 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
                 }
                 if (vi < 0) { ok = false; break; }
                 const size_t slot = slot_of(sl, k, lane);
-                ent[slot] = (uint32_t)(16 * vi) | ((uint32_t)(16 * c) << 16);
+                // texture-path variants (sell_uses_tex): the value index itself
+                ent[slot] = (uint32_t)(use_tex ? vi : 16 * vi) | ((uint32_t)(16 * c) << 16);
                 for (int t = 0; t < nt1; ++t) {
                     const qtm_csr* m = tds[t];
                     int ti = 0;
@@ -488,6 +491,20 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         P.sell_w = d_w;
         P.sell_td = 0;
         P.sell_td_dict_n = 0;
+        P.sell_tex = 0;
+        if (use_tex) {
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = d_dict;
+            rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+            rd.res.linear.sizeInBytes = sizeof(double2) * dict.size();
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            cudaTextureObject_t tex = 0;
+            CUDA_TRY(cudaCreateTextureObject(&tex, &rd, &td, nullptr));
+            P.sell_tex = (unsigned long long)tex;
+            p->sell_tex = tex;
+        }
         if (nt1) {
             double2* d_tdict = nullptr;
             uint16_t* d_tent = nullptr;
@@ -647,6 +664,7 @@ void free_problem(qtm_problem* p) {
     p->psi_slot.release(s); p->psi_out.release(s);
     p->bdf_ws.release(s);
     if (s) cudaStreamSynchronize(s);
+    if (p->sell_tex) cudaDestroyTextureObject(p->sell_tex);
     for (auto& e : p->ev) if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
     delete p;
@@ -882,7 +900,8 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         std::vector<const qtm_csr*> tds;
         if (var.td)
             for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
-        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds);
+        rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds,
+                        sell_uses_tex(var.threads, var.comps, var.reg_rows, var.td != 0));
     }
     if (rc == QTM_OK && p->method == 0 && !var.small) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->method == 0 && var.tm) {

@@ -89,6 +89,10 @@ struct DevProblem {
     int sell_entries, sell_dict_n;
     const uint32_t* sell_ent;
     const double2* sell_dict;
+    // variants with sell_uses_tex(): the dictionary as a linear texture over
+    // sell_dict; the entries' low half is then the value INDEX instead of its
+    // byte offset
+    unsigned long long sell_tex;
     const int* sell_off;    // [NT/32] first entry slot of each warp (SellSlots)
     const int* sell_w;      // [DP/32] width of each slice (uniform over a warp's E slices)
     // TD variants: the SELL above is built on the union pattern of G0 and
@@ -362,11 +366,39 @@ __device__ __forceinline__ double2 sell_val(const char* db, uint32_t u) {
 __device__ __forceinline__ double2 sell_x(const char* xb, uint32_t u) {
     return *reinterpret_cast<const double2*>(xb + (u >> 16));
 }
-template <int NT, int E, int PF>
+// QTM_SELL_TEX: the dictionary values come through the TEXTURE pipe
+// (tex1Dfetch over the dictionary in HBM, L1/TEX-cached) instead of shared
+// memory.  The shared-memory (LSU) data pipe is this kernel's binding
+// resource and the texture pipe runs beside it: measured with
+// tools/smem_bench.cu, a 16-byte gather from shared memory plus a 16-byte
+// dictionary load from shared memory cost 10 SM-cycles per warp, the gather
+// plus a tex1Dfetch<int4> cost 8 (the fetch alone: 8, fully overlapped).
+// Where it pays (measured A/B, bitwise the same results): the three-warp
+// one-row-per-thread variants at 8 CTAs per SM (c3, (96, 1, 9): 486 -> 452 ms
+// per step) -- enough warps to hide the texture latency, and a SpMV short
+// enough that the fetches of one column cover most of it.  Elsewhere it does
+// not: the wide variants lose (c4 109 -> 127 ms, c5 2 810 -> 3 123 ms per
+// 4 096 trajectories even with the values prefetched a column ahead: 16 warps
+// per SM do not cover ~500 cycles per column), and the other small shapes are
+// mixed on 512-trajectory samples ((64, 1, 13) on c2 13.1 -> 15.2 ms,
+// (32, 1, 13) 13.1 -> 11.5, (128, 1, 13) on c3 30.4 -> 30.9), so they keep the
+// dictionary in shared memory.
+#ifndef QTM_SELL_TEX
+#define QTM_SELL_TEX 1
+#endif
+// the variants whose dictionary goes through the texture pipe
+__host__ __device__ constexpr bool sell_uses_tex(int threads, int comps, int reg_rows, bool td) {
+    return QTM_SELL_TEX && comps == 1 && reg_rows > 0 && threads == 96 && !td;
+}
+__device__ __forceinline__ double2 tex_val(unsigned long long tex, uint32_t u) {
+    const int4 t = tex1Dfetch<int4>((cudaTextureObject_t)tex, (int)(u & 0xFFFFu));
+    return make_double2(__hiloint2double(t.y, t.x), __hiloint2double(t.w, t.z));
+}
+template <int NT, int E, int PF, bool TEX = false>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
                                           const double2* __restrict__ dict, int woff,
                                           int width, const double2* __restrict__ x,
-                                          double2 (&out)[E]) {
+                                          double2 (&out)[E], unsigned long long tex = 0) {
     using S = SellSlots<E>;
     const int lane = threadIdx.x & 31;
     const char* const xb = reinterpret_cast<const char*>(x);
@@ -375,7 +407,34 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
     double sr[E], si[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; }
-    if constexpr (PF == 0) {
+    if constexpr (TEX) {
+        // values one column ahead through the texture pipe (long latency), the
+        // gathered x just in time from shared memory
+        if (width > 0) {
+            uint32_t u[E];
+            double2 v[E];
+            S::load(p, u);
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = tex_val(tex, u[e]);
+            QTM_SPMV_UNROLL_PRAGMA
+            for (int k = 1; k < width; ++k) {
+                double2 xv[E], vn[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) xv[e] = sell_x(xb, u[e]);
+                p += 32 * E;
+                S::load(p, u);
+#pragma unroll
+                for (int e = 0; e < E; ++e) vn[e] = tex_val(tex, u[e]);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    cmac(sr[e], si[e], v[e], xv[e]);
+                    v[e] = vn[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) cmac(sr[e], si[e], v[e], sell_x(xb, u[e]));
+        }
+    } else if constexpr (PF == 0) {
 #pragma unroll (E >= 4 ? 1 : 2)
         for (int k = 0; k < width; ++k) {
             uint32_t u[E];
@@ -1375,7 +1434,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV(xs, f)                                                         \
     do {                                                                     \
         if (P.sell_mode) {                                                   \
-            sell_spmv<NT, E, QTM_SPMV_PF(RREG)>(s_ent, s_dict, goff, gwidth, (xs), f); \
+            sell_spmv<NT, E, QTM_SPMV_PF(RREG), sell_uses_tex(NT, E, RREG, TD)>(s_ent, s_dict, goff, gwidth, (xs), f, P.sell_tex); \
         } else {                                                             \
             _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
                 f[e] = ACT(e) ? row_dot(P.g, II(e), (xs)) : make_double2(0.0, 0.0); \

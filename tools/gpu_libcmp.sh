@@ -6,7 +6,7 @@
 cd ${GRAFT_REPO_ROOT:-.}; mkdir -p gpurun_out
 TAG=$1; LT=$2
 P=$PWD/paper_1810_03047_b200
-SPECS="c4:296:39 c4:148:22 c5:128:27 c3:512:12 c2:512:17 c1:500:0 c4td:148:36 c4:128:6 c5:64:26 c4:64:38"
+SPECS="c4:296:39 c4:148:22 c5:128:27 c3:512:12 c2:512:17 c1:500:0 c4td:148:36 c4:128:6 c5:64:26 c4:64:38 c3:512:3 c3:256:13 c2:512:1 c2:512:0"
 QTM_LIB=$P/libqtm.so timeout 900 python tools/lib_dump.py dump gpurun_out/${TAG}_base.npz $SPECS > gpurun_out/${TAG}_dump_base.log 2>&1
 QTM_LIB=$P/libqtm_$LT.so timeout 900 python tools/lib_dump.py dump gpurun_out/${TAG}_new.npz $SPECS > gpurun_out/${TAG}_dump_new.log 2>&1
 python tools/lib_dump.py cmp gpurun_out/${TAG}_base.npz gpurun_out/${TAG}_new.npz > gpurun_out/${TAG}_cmp.log 2>&1
