@@ -370,9 +370,11 @@ __device__ __forceinline__ double2 sell_x(const char* xb, uint32_t u) {
 // (tex1Dfetch over the dictionary in HBM, L1/TEX-cached) instead of shared
 // memory.  The shared-memory (LSU) data pipe is this kernel's binding
 // resource and the texture pipe runs beside it: measured with
-// tools/smem_bench.cu, a 16-byte gather from shared memory plus a 16-byte
-// dictionary load from shared memory cost 10 SM-cycles per warp, the gather
-// plus a tex1Dfetch<int4> cost 8 (the fetch alone: 8, fully overlapped).
+// tools/smem_bench.cu, a 16-byte gather plus a 16-byte dictionary load from
+// shared memory cost 4 + 4 SM-cycles per warp on the LSU pipe; with the value
+// as a tex1Dfetch<int4> the pair still takes 8 (the fetch alone: 8), but only
+// 4 of them on the LSU pipe -- the fetch overlaps the shared-memory load
+// completely.
 // Where it pays (measured A/B, bitwise the same results): the three-warp
 // one-row-per-thread variants at 8 CTAs per SM (c3, (96, 1, 9): 486 -> 452 ms
 // per step) -- enough warps to hide the texture latency, and a SpMV short

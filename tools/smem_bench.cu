@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
     __syncthreads();
     int4 acc = make_int4(0, 0, 0, 0);
     int idx;
-    if (MODE == 1 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8) idx = lane;
+    if (MODE == 1 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8 || MODE >= 9) idx = lane;
     else if (MODE == 2) idx = 5;
     else idx = (lane * 7) & 7;  // 8 distinct
     long long t0 = clock64();
@@ -48,12 +48,29 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
             } else if (MODE == 6) {
                 const int4 v = buf[(idx + 32 * u + o1) & 2047];
                 const int4 w = tex1Dfetch<int4>(tex, (((lane * 7) & 7) + 8 * u + o2) & 63);
-                acc.x ^= v.x; acc.y ^= w.y; acc.z ^= v.z; acc.w ^= w.w;
+                acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
+            } else if (MODE == 9) {
+                // two conflict-free LDS.128 with distinct addresses
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int4 w = buf[(lane + 32 * u + 1024 + o2) & 2047];
+                acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
+            } else if (MODE == 10) {
+                // gather + the value as two LDS.64 halves from an 8-entry table
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int2* const h = reinterpret_cast<const int2*>(buf);
+                const int2 a = h[(((lane * 7) & 7) + 8 * u + o2) & 63];
+                const int2 b = h[((((lane * 7) & 7) + 8 * u + o2) & 63) + 2048];
+                acc.x ^= v.x ^ a.x; acc.y ^= v.y ^ a.y; acc.z ^= v.z ^ b.x; acc.w ^= v.w ^ b.y;
+            } else if (MODE == 11) {
+                // gather + one-address LDS.128 (a warp-uniform value)
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int4 w = buf[(5 + 8 * u + o2) & 63];
+                acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
             } else if (MODE == 4) {
                 // two LDS.128 per step (x + value, both through shared memory)
                 const int4 v = buf[(idx + 32 * u + o1) & 2047];
                 const int4 w = buf[(((lane * 7) & 7) + 8 * u + o2) & 63];
-                acc.x ^= v.x; acc.y ^= w.y; acc.z ^= v.z; acc.w ^= w.w;
+                acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
             }
         }
     }
@@ -105,6 +122,9 @@ int main() {
     run<7>("LDS.64, 32 distinct addresses", tex, d_out, d_sink, sms);
     run<8>("LDS.32, 32 distinct addresses", tex, d_out, d_sink, sms);
     run<4>("LDS.128 distinct + LDS.128 8-address (x + value)", tex, d_out, d_sink, sms);
+    run<9>("LDS.128 distinct + LDS.128 distinct", tex, d_out, d_sink, sms);
+    run<10>("LDS.128 distinct + 2 x LDS.64 8-address (split value)", tex, d_out, d_sink, sms);
+    run<11>("LDS.128 distinct + LDS.128 one address", tex, d_out, d_sink, sms);
     run<5>("tex1Dfetch<int4>, 8 distinct addresses", tex, d_out, d_sink, sms);
     run<6>("LDS.128 distinct + tex1Dfetch<int4> (x + value via TEX)", tex, d_out, d_sink, sms);
     return 0;
