@@ -15,6 +15,20 @@
 constexpr int ITERS = 4096;
 constexpr int UNR = 8;
 
+// predicated shared loads (the predicate is per lane; inactive lanes keep the default)
+__device__ __forceinline__ int4 lds128_if(const void* p, int on, int4 d) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("{ .reg .pred q; setp.ne.s32 q, %5, 0; @q ld.shared.v4.s32 {%0,%1,%2,%3}, [%4]; }"
+                 : "+r"(d.x), "+r"(d.y), "+r"(d.z), "+r"(d.w) : "r"(a), "r"(on));
+    return d;
+}
+__device__ __forceinline__ int2 lds64_if(const void* p, int on, int2 d) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("{ .reg .pred q; setp.ne.s32 q, %3, 0; @q ld.shared.v2.s32 {%0,%1}, [%2]; }"
+                 : "+r"(d.x), "+r"(d.y) : "r"(a), "r"(on));
+    return d;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* out, int4* sink) {
     __shared__ int4 buf[2048];  // 32 KB
@@ -23,7 +37,7 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
     __syncthreads();
     int4 acc = make_int4(0, 0, 0, 0);
     int idx;
-    if (MODE == 1 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8 || MODE >= 9) idx = lane;
+    if (MODE == 1 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8 || MODE >= 9) idx = lane;  // (modes >= 12 use idx only for the gather)
     else if (MODE == 2) idx = 5;
     else idx = (lane * 7) & 7;  // 8 distinct
     long long t0 = clock64();
@@ -66,6 +80,41 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
                 const int4 v = buf[(idx + 32 * u + o1) & 2047];
                 const int4 w = buf[(5 + 8 * u + o2) & 63];
                 acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
+            } else if (MODE == 12 || MODE == 13) {
+                // LDS.64: one address / 8 distinct addresses
+                const int2* const h = reinterpret_cast<const int2*>(buf);
+                const int2 a = h[((MODE == 12 ? 5 : ((lane * 7) & 7)) + 8 * u + o2) & 63];
+                acc.x ^= a.x; acc.y ^= a.y;
+            } else if (MODE >= 14 && MODE <= 17) {
+                // predicated LDS.128, 8-entry dictionary addresses; active lanes:
+                // 14: popcount(lane) == 2 (10 lanes, in every quarter-warp)
+                // 15: lanes 0..7 (one quarter-warp)   16: lane 0   17: none
+                const int on = MODE == 14 ? (__popc(lane) == 2) : MODE == 15 ? (lane < 8) : MODE == 16 ? (lane == 0) : (acc.w == 0x7ffffff1);
+                const int4 w = lds128_if(&buf[(((lane * 7) & 7) + 8 * u + o2) & 63], on, make_int4(1, 2, 3, 4));
+                acc.x ^= w.x; acc.y ^= w.y; acc.z ^= w.z; acc.w ^= w.w;
+            } else if (MODE == 18 || MODE == 19) {
+                // gather + LDS.64 value (one address / 8 distinct)
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int2* const h = reinterpret_cast<const int2*>(buf);
+                const int2 a = h[((MODE == 18 ? 5 : ((lane * 7) & 7)) + 8 * u + o2) & 63];
+                acc.x ^= v.x ^ a.x; acc.y ^= v.y ^ a.y; acc.z ^= v.z; acc.w ^= v.w;
+            } else if (MODE == 20 || MODE == 21 || MODE == 22) {
+                // gather + per-lane choice: complex value (LDS.128) on the lanes with
+                // popcount(lane) == 2 [20] / lanes 0..7 [21] / none [22], imaginary-only
+                // value (LDS.64) on the others; both from 8-entry dictionaries
+                const int on = MODE == 20 ? (__popc(lane) == 2) : MODE == 21 ? (lane < 8) : (acc.w == 0x7ffffff1);
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int2* const h = reinterpret_cast<const int2*>(buf);
+                const int j = (((lane * 7) & 7) + 8 * u + o2) & 63;
+                const int4 w = lds128_if(&buf[j], on, make_int4(0, 0, 0, 0));
+                const int2 a = lds64_if(&h[j + 2048], !on, make_int2(w.z, w.w));
+                acc.x ^= v.x ^ w.x; acc.y ^= v.y ^ w.y; acc.z ^= v.z ^ a.x; acc.w ^= v.w ^ a.y;
+            } else if (MODE == 23) {
+                // gather + dominant value in registers, dictionary LDS.128 only on the
+                // lanes with popcount(lane) == 2
+                const int4 v = buf[(idx + 32 * u + o1) & 2047];
+                const int4 w = lds128_if(&buf[(((lane * 7) & 7) + 8 * u + o2) & 63], __popc(lane) == 2, make_int4(o2, 2, 3, 4));
+                acc.x ^= v.x ^ w.w; acc.y ^= v.y ^ w.z; acc.z ^= v.z ^ w.y; acc.w ^= v.w ^ w.x;
             } else if (MODE == 4) {
                 // two LDS.128 per step (x + value, both through shared memory)
                 const int4 v = buf[(idx + 32 * u + o1) & 2047];
@@ -77,6 +126,56 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
     long long t1 = clock64();
     if (tid == 0) out[blockIdx.x] = t1 - t0;
     if (acc.x == 0x7fffffff) sink[0] = acc;
+}
+
+// Predicated loads, pipe-bound form: the address and the predicate are set up
+// outside the timed loop and each step is one predicated load plus one XOR, so
+// the issue slots (16 warps per SM: 4 instructions per SM-cycle) stay far from
+// binding.  WIDTH = 16 / 8 bytes; PAT = which lanes are on:
+//   0 all, 1 popcount(lane) == 2 (10 lanes, every quarter-warp), 2 lanes 0..7,
+//   3 lane 0, 4 none, 5 lanes 0..15, 6 even lanes
+template <int WIDTH, int PAT, bool SAME>
+__global__ void __launch_bounds__(512, 1) kp(long long* out, int4* sink) {
+    __shared__ int4 buf[2048];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int i = tid; i < 2048; i += blockDim.x) buf[i] = make_int4(i, i + 1, i + 2, i + 3);
+    __syncthreads();
+    const int on = PAT == 0 ? 1 : PAT == 1 ? (__popc(lane) == 2) : PAT == 2 ? (lane < 8) : PAT == 3 ? (lane == 0)
+                 : PAT == 4 ? (tid == 4096) : PAT == 5 ? (lane < 16) : ((lane & 1) == 0);
+    const unsigned a0 = (unsigned)__cvta_generic_to_shared(buf) + (SAME ? 80u : (unsigned)(((lane * 7) & 7) * 16));
+    int acc = 0;
+    long long t0 = clock64();
+    for (int it = 0; it < ITERS; ++it) {
+        const unsigned a = a0 + ((unsigned)(acc & 32) << 4);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            int x = 1, y = 2, z = 3, w = 4;
+            if (WIDTH == 16)
+                asm volatile("{ .reg .pred q; setp.ne.s32 q, %5, 0; @q ld.shared.v4.s32 {%0,%1,%2,%3}, [%4+%6]; }"
+                             : "+r"(x), "+r"(y), "+r"(z), "+r"(w) : "r"(a), "r"(on), "n"(0));
+            else
+                asm volatile("{ .reg .pred q; setp.ne.s32 q, %3, 0; @q ld.shared.v2.s32 {%0,%1}, [%2+%4]; }"
+                             : "+r"(x), "+r"(y) : "r"(a), "r"(on), "n"(0));
+            acc ^= WIDTH == 16 ? (x ^ y ^ z ^ w) : (x ^ y);  // every loaded word consumed (or ptxas narrows the load)
+        }
+    }
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x] = t1 - t0;
+    if (acc == 0x7fffffff) sink[0] = make_int4(acc, 0, 0, 0);
+}
+template <int WIDTH, int PAT, bool SAME>
+static void runp(const char* name, long long* d_out, int4* d_sink, int sms) {
+    kp<WIDTH, PAT, SAME><<<sms, 512>>>(d_out, d_sink);
+    cudaDeviceSynchronize();
+    kp<WIDTH, PAT, SAME><<<sms, 512>>>(d_out, d_sink);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
+    long long h[256];
+    cudaMemcpy(h, d_out, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < sms; ++i) avg += (double)h[i];
+    avg /= sms;
+    printf("%-58s %8.2f SM-cycles per warp step (16 warps/SM)\n", name, avg / ((double)ITERS * UNR * 16));
 }
 
 template <int MODE>
@@ -125,6 +224,32 @@ int main() {
     run<9>("LDS.128 distinct + LDS.128 distinct", tex, d_out, d_sink, sms);
     run<10>("LDS.128 distinct + 2 x LDS.64 8-address (split value)", tex, d_out, d_sink, sms);
     run<11>("LDS.128 distinct + LDS.128 one address", tex, d_out, d_sink, sms);
+    run<12>("LDS.64, one address for the warp", tex, d_out, d_sink, sms);
+    run<13>("LDS.64, 8 distinct addresses", tex, d_out, d_sink, sms);
+    run<14>("@p LDS.128 8-address, 10 lanes on (every quarter-warp)", tex, d_out, d_sink, sms);
+    run<15>("@p LDS.128 8-address, lanes 0..7 on", tex, d_out, d_sink, sms);
+    run<16>("@p LDS.128 8-address, lane 0 on", tex, d_out, d_sink, sms);
+    run<17>("@p LDS.128 8-address, no lane on", tex, d_out, d_sink, sms);
+    run<18>("LDS.128 distinct + LDS.64 one address", tex, d_out, d_sink, sms);
+    run<19>("LDS.128 distinct + LDS.64 8-address", tex, d_out, d_sink, sms);
+    run<20>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, 10 lanes complex", tex, d_out, d_sink, sms);
+    run<21>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, lanes 0..7 complex", tex, d_out, d_sink, sms);
+    run<22>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, no lane complex", tex, d_out, d_sink, sms);
+    run<23>("LDS.128 distinct + @p LDS.128 10 lanes (dominant value in registers)", tex, d_out, d_sink, sms);
+    runp<16, 0, false>("@p LDS.128 8-address, all lanes on [pipe-bound form]", d_out, d_sink, sms);
+    runp<16, 1, false>("@p LDS.128 8-address, 10 lanes on, every quarter", d_out, d_sink, sms);
+    runp<16, 5, false>("@p LDS.128 8-address, lanes 0..15 on", d_out, d_sink, sms);
+    runp<16, 6, false>("@p LDS.128 8-address, even lanes on", d_out, d_sink, sms);
+    runp<16, 2, false>("@p LDS.128 8-address, lanes 0..7 on", d_out, d_sink, sms);
+    runp<16, 3, false>("@p LDS.128 8-address, lane 0 on", d_out, d_sink, sms);
+    runp<16, 4, false>("@p LDS.128 8-address, no lane on", d_out, d_sink, sms);
+    runp<16, 0, true>("@p LDS.128 one address, all lanes on", d_out, d_sink, sms);
+    runp<16, 1, true>("@p LDS.128 one address, 10 lanes on", d_out, d_sink, sms);
+    runp<8, 0, false>("@p LDS.64 8-address, all lanes on", d_out, d_sink, sms);
+    runp<8, 1, false>("@p LDS.64 8-address, 10 lanes on, every quarter", d_out, d_sink, sms);
+    runp<8, 5, false>("@p LDS.64 8-address, lanes 0..15 on", d_out, d_sink, sms);
+    runp<8, 4, false>("@p LDS.64 8-address, no lane on", d_out, d_sink, sms);
+    runp<8, 0, true>("@p LDS.64 one address, all lanes on", d_out, d_sink, sms);
     run<5>("tex1Dfetch<int4>, 8 distinct addresses", tex, d_out, d_sink, sms);
     run<6>("LDS.128 distinct + tex1Dfetch<int4> (x + value via TEX)", tex, d_out, d_sink, sms);
     return 0;
