@@ -379,7 +379,7 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
 // L2 (row_dot).
 int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
                size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {},
-               bool use_tex = false) {
+               bool use_tex = false, bool use_dom = false) {
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
@@ -438,6 +438,24 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         };
         std::vector<double2> dict(1, make_double2(0.0, 0.0)), tdict(1, make_double2(0.0, 0.0));
         std::map<Key, int> index, tindex;
+        // sell_uses_dom variants: the purely imaginary value (+0.0, b) that
+        // makes up at least half of the stored entries, if there is one
+        bool dom_on = false;
+        Key dom_key{0, 0};
+        if (use_dom && !use_tex && nt1 == 0) {
+            std::map<Key, int64_t> freq;
+            const int64_t nnz = g.row_ptr[n];
+            for (int64_t j = 0; j < nnz; ++j) {
+                Key key;
+                memcpy(&key.a, &g.values[2 * j], 8);
+                memcpy(&key.b, &g.values[2 * j + 1], 8);
+                if (key.a == 0) ++freq[key];  // re is +0.0 bit for bit
+            }
+            int64_t best = 0;
+            for (const auto& kv : freq)
+                if (kv.second > best) { best = kv.second; dom_key = kv.first; }
+            dom_on = nnz > 0 && 2 * best >= nnz;
+        }
         std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: x[0] * dict[0] (= 0)
         const size_t nslot = (size_t)std::max(total, 1);
         std::vector<uint16_t> tent((size_t)nt1 * nslot, 0);
@@ -450,12 +468,21 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             for (size_t k = 0; k < cols[i].size() && ok; ++k) {
                 const int64_t c = cols[i][k];
                 int vi = 0;  // a G_k-only slot: G0 contributes an exact zero
+                bool is_dom = false;
                 if (j0 < g.row_ptr[i + 1] && g.col_ind[j0] == c) {
-                    vi = lookup(index, dict, g.values[2 * j0], g.values[2 * j0 + 1]);
+                    Key key;
+                    memcpy(&key.a, &g.values[2 * j0], 8);
+                    memcpy(&key.b, &g.values[2 * j0 + 1], 8);
+                    is_dom = dom_on && key.a == dom_key.a && key.b == dom_key.b;
+                    if (!is_dom) vi = lookup(index, dict, g.values[2 * j0], g.values[2 * j0 + 1]);
                     ++j0;
                 }
                 if (vi < 0) { ok = false; break; }
                 const size_t slot = slot_of(sl, k, lane);
+                if (is_dom) {  // bit 0: the value is DevProblem::sell_dom
+                    ent[slot] = 1u | ((uint32_t)(16 * c) << 16);
+                    continue;
+                }
                 // texture-path variants (sell_uses_tex): the value index itself
                 ent[slot] = (uint32_t)(use_tex ? vi : 16 * vi) | ((uint32_t)(16 * c) << 16);
                 for (int t = 0; t < nt1; ++t) {
@@ -492,6 +519,9 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         P.sell_td = 0;
         P.sell_td_dict_n = 0;
         P.sell_tex = 0;
+        P.sell_dom_on = dom_on ? 1 : 0;
+        P.sell_dom = 0.0;
+        if (dom_on) memcpy(&P.sell_dom, &dom_key.b, 8);
         if (use_tex) {
             cudaResourceDesc rd{};
             rd.resType = cudaResourceTypeLinear;
@@ -900,8 +930,10 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         std::vector<const qtm_csr*> tds;
         if (var.td)
             for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
+        const bool dom_env = !(getenv("QTM_DOM") && atoi(getenv("QTM_DOM")) == 0);  // A/B: QTM_DOM=0
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds,
-                        sell_uses_tex(var.threads, var.comps, var.reg_rows, var.td != 0));
+                        sell_uses_tex(var.threads, var.comps, var.reg_rows, var.td != 0),
+                        dom_env && sell_uses_dom(var.threads, var.comps, var.reg_rows, var.td != 0));
     }
     if (rc == QTM_OK && p->method == 0 && !var.small) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->method == 0 && var.tm) {

@@ -93,6 +93,12 @@ struct DevProblem {
     // sell_dict; the entries' low half is then the value INDEX instead of its
     // byte offset
     unsigned long long sell_tex;
+    // variants with sell_uses_dom(): when one purely imaginary value (0, b)
+    // makes up most of G's stored entries (every off-diagonal of c4's Ising
+    // chain is i h), its entries carry bit 0 instead of a dictionary offset
+    // and take the value from this field: no dictionary load for them
+    int sell_dom_on;
+    double sell_dom;
     const int* sell_off;    // [NT/32] first entry slot of each warp (SellSlots)
     const int* sell_w;      // [DP/32] width of each slice (uniform over a warp's E slices)
     // TD variants: the SELL above is built on the union pattern of G0 and
@@ -396,11 +402,32 @@ __device__ __forceinline__ double2 tex_val(unsigned long long tex, uint32_t u) {
     const int4 t = tex1Dfetch<int4>((cudaTextureObject_t)tex, (int)(u & 0xFFFFu));
     return make_double2(__hiloint2double(t.y, t.x), __hiloint2double(t.w, t.z));
 }
-template <int NT, int E, int PF, bool TEX = false>
+// QTM_SELL_DOM: the dominant purely imaginary value of G comes from the kernel
+// parameters instead of the dictionary (DevProblem::sell_dom).  The load is
+// predicated per lane on bit 0 of the entry; the product is formed by the same
+// cmac from the same bits (re = +0.0), so the results are bitwise unchanged.
+#ifndef QTM_SELL_DOM
+#define QTM_SELL_DOM 1
+#endif
+// the variants that take it: the wide register / TMEM variants (several rows
+// per thread, pipelined SpMV), whose bound is the shared-memory data pipe
+__host__ __device__ constexpr bool sell_uses_dom(int threads, int comps, int reg_rows, bool td) {
+    return QTM_SELL_DOM && comps > 1 && reg_rows > 0 && !td && !sell_uses_tex(threads, comps, reg_rows, td);
+}
+__device__ __forceinline__ double2 sell_val_dom(uint32_t dbs, uint32_t u, double dom) {
+    double2 v = make_double2(0.0, dom);
+    asm("{\n\t.reg .pred q;\n\t.reg .b32 t;\n\tand.b32 t, %3, 1;\n\tsetp.eq.u32 q, t, 0;\n\t"
+        "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
+        : "+d"(v.x), "+d"(v.y)
+        : "r"(dbs + (u & 0xFFFFu)), "r"(u));
+    return v;
+}
+template <int NT, int E, int PF, bool TEX = false, bool DOM = false>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
                                           const double2* __restrict__ dict, int woff,
                                           int width, const double2* __restrict__ x,
-                                          double2 (&out)[E], unsigned long long tex = 0) {
+                                          double2 (&out)[E], unsigned long long tex = 0,
+                                          int dom_on = 0, double dom = 0.0) {
     using S = SellSlots<E>;
     const int lane = threadIdx.x & 31;
     const char* const xb = reinterpret_cast<const char*>(x);
@@ -454,6 +481,29 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
             const double2 v = sell_val(db, u), xv = sell_x(xb, u);
             u = p[kn * 32];
             cmac(sr[0], si[0], v, xv);
+        }
+    } else if (DOM && dom_on) {
+        // the same pipelined loop with the dominant value's entries served
+        // from `dom` (a separate copy, so problems without one pay nothing)
+        if (width > 0) {
+            const uint32_t dbs = (uint32_t)__cvta_generic_to_shared(db);
+            uint32_t u[E];
+            S::load(p, u);
+            QTM_SPMV_UNROLL_PRAGMA
+            for (int k = 1; k < width; ++k) {
+                double2 v[E], xv[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    v[e] = sell_val_dom(dbs, u[e], dom);
+                    xv[e] = sell_x(xb, u[e]);
+                }
+                p += 32 * E;
+                S::load(p, u);
+#pragma unroll
+                for (int e = 0; e < E; ++e) cmac(sr[e], si[e], v[e], xv[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) cmac(sr[e], si[e], sell_val_dom(dbs, u[e], dom), sell_x(xb, u[e]));
         }
     } else if (width > 0) {
         uint32_t u[E];
@@ -1436,7 +1486,8 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV(xs, f)                                                         \
     do {                                                                     \
         if (P.sell_mode) {                                                   \
-            sell_spmv<NT, E, QTM_SPMV_PF(RREG), sell_uses_tex(NT, E, RREG, TD)>(s_ent, s_dict, goff, gwidth, (xs), f, P.sell_tex); \
+            sell_spmv<NT, E, QTM_SPMV_PF(RREG), sell_uses_tex(NT, E, RREG, TD), sell_uses_dom(NT, E, RREG, TD)>( \
+                s_ent, s_dict, goff, gwidth, (xs), f, P.sell_tex, P.sell_dom_on, P.sell_dom); \
         } else {                                                             \
             _Pragma("unroll") for (int e = 0; e < E; ++e)                    \
                 f[e] = ACT(e) ? row_dot(P.g, II(e), (xs)) : make_double2(0.0, 0.0); \
