@@ -363,7 +363,7 @@ def main(argv=None):
 
     from paper_1810_03047_b200 import configs, native
     from paper_1810_03047_b200.configs import N_TRAJECTORIES
-    from paper_1810_03047_b200.engine import (smem_model, DeviceProblem, autotune_variant, bytes_model,
+    from paper_1810_03047_b200.engine import (smem_model, spmv_value_bytes, DeviceProblem, autotune_variant, bytes_model,
                                               flops_model, run_sharded, shard_range, stats_dict)
     from paper_1810_03047_b200.packing import pack_problem
 
@@ -474,13 +474,17 @@ def main(argv=None):
         n_sm = torch.cuda.get_device_properties(local).multi_processor_count
         mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965
         smem_peak = 128.0 * n_sm * mhz * 1e6 / 1e12
-        smem_tbs = smem_model(st, packed) / (k_ms * 1e-3) / 1e12
+        shape = native.variants()[outs[-1].variant]
+        vbytes = spmv_value_bytes(packed, shape) / max(packed.g.nnz, 1)
+        smem_tbs = smem_model(st, packed, shape) / (k_ms * 1e-3) / 1e12
         prof = profiled_smem_pct(args.config) or {}
         smem = {"achieved_tbs": smem_tbs, "peak_tbs": smem_peak, "frac": smem_tbs / smem_peak,
-                "model": "corr_iters (36 nnz + 40 d) + attempts 16 d bytes (engine.smem_model)",
+                "model": f"corr_iters ({20 + vbytes:.1f} nnz + 40 d) + attempts 16 d bytes (engine.smem_model)",
+                "value_bytes_per_nonzero": vbytes,
                 "peak_source": f"128 B/clk/SM x {n_sm} SMs x {mhz} MHz (clock sampled under load)",
                 "ncu_pipe_pct": prof.get("pct"), "ncu_source": prof.get("source"),
-                "note": "the staged-operator SpMV streams 36 B per nonzero from shared memory; "
+                "note": "the staged-operator SpMV streams an entry word, a gathered x and a dictionary value "
+                        "(16 B; 8 B purely imaginary; none for the dominant value) per nonzero from shared memory; "
                         "ncu_pipe_pct is the measured l1tex shared-memory wavefront utilisation "
                         "of the committed capture (all shared-memory traffic, not the model's)"}
 

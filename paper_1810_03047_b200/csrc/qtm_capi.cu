@@ -379,7 +379,7 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
 // L2 (row_dot).
 int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
                size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {},
-               bool use_tex = false, bool use_dom = false) {
+               bool use_tex = false, int use_dom = 0) {
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
@@ -430,7 +430,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             memcpy(&key.b, &im, 8);
             auto it = index.find(key);
             if (it == index.end()) {
-                if (dict.size() >= 4096) return -1;  // too many distinct values
+                if (dict.size() >= 4096) return -1;  // too many distinct values (16-bit byte offsets)
                 it = index.emplace(key, (int)dict.size()).first;
                 dict.push_back(make_double2(re, im));
             }
@@ -442,24 +442,60 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         // makes up at least half of the stored entries, if there is one
         bool dom_on = false;
         Key dom_key{0, 0};
+        int64_t n_imag_other = 0;  // purely imaginary entries besides the dominant value
         if (use_dom && !use_tex && nt1 == 0) {
             std::map<Key, int64_t> freq;
             const int64_t nnz = g.row_ptr[n];
+            int64_t n_imag = 0;
             for (int64_t j = 0; j < nnz; ++j) {
                 Key key;
                 memcpy(&key.a, &g.values[2 * j], 8);
                 memcpy(&key.b, &g.values[2 * j + 1], 8);
-                if (key.a == 0) ++freq[key];  // re is +0.0 bit for bit
+                if (key.a == 0) { ++freq[key]; ++n_imag; }  // re is +0.0 bit for bit
             }
             int64_t best = 0;
             for (const auto& kv : freq)
                 if (kv.second > best) { best = kv.second; dom_key = kv.first; }
-            dom_on = nnz > 0 && 2 * best >= nnz;
+            dom_on = (use_dom & 1) && nnz > 0 && 2 * best >= nnz;
+            n_imag_other = n_imag - (dom_on ? best : 0);
+            // 8-byte values only where they are a sizeable share of the entries
+            // (c5: 79 %); a handful (c4: one diagonal entry) stays complex, so the
+            // kernel runs the loop without the second predicated load
+            if (4 * n_imag_other < nnz) n_imag_other = 0;
         }
         std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: x[0] * dict[0] (= 0)
         const size_t nslot = (size_t)std::max(total, 1);
         std::vector<uint16_t> tent((size_t)nt1 * nslot, 0);
         bool ok = true;
+        // sell_uses_dom variants also keep every other purely imaginary value
+        // (+0.0, b) as ONE double behind the complex dictionary (entry bit 1:
+        // an 8-byte load, half the shared-memory wavefronts of a 16-byte one),
+        // and align the diagonal -- normally the only entry with a real part
+        // -- to one position per warp by inserting exact-zero entries before
+        // it where the warp's width has room, so that whole columns of a warp
+        // are 8-byte loads.  An inserted entry adds (+0.0, 0.0) * x[0] at its
+        // place in the row's sum, exactly as the padding behind a short row does.
+        const bool imag_on = (use_dom & 2) && !use_tex && nt1 == 0 && n_imag_other > 0;
+        std::vector<double> idict(1, 0.0);  // [0] = 0.0: inserted entries and padding
+        std::map<uint64_t, int> iindex;
+        std::vector<uint32_t> ikind(imag_on ? nslot : 0, 0u);  // 1 = the low half is an idict index
+        std::vector<int> prepad(imag_on ? n : 0, 0);
+        bool any_imag = false;
+        if (imag_on) {
+            // diagonal position per row; target = the largest one among the rows a warp walks
+            std::vector<int> dpos(n, -1), target(nw, 0);
+            for (int64_t i = 0; i < n; ++i) {
+                for (size_t k = 0; k < cols[i].size(); ++k)
+                    if (cols[i][k] == i) dpos[i] = (int)k;
+                if (dpos[i] >= 0) target[(i / 32) % nw] = std::max(target[(i / 32) % nw], dpos[i]);
+            }
+            for (int64_t i = 0; i < n; ++i) {
+                if (dpos[i] < 0) continue;
+                const int sl = (int)(i / 32);
+                prepad[i] = std::min(target[sl % nw] - dpos[i], width[sl] - (int)cols[i].size());
+            }
+            for (uint32_t& k : ikind) k = 1u;  // padding everywhere: idict[0]
+        }
         for (int64_t i = 0; i < n && ok; ++i) {
             const int sl = (int)(i / 32), lane = (int)(i % 32);
             int64_t j0 = g.row_ptr[i];
@@ -468,23 +504,41 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             for (size_t k = 0; k < cols[i].size() && ok; ++k) {
                 const int64_t c = cols[i][k];
                 int vi = 0;  // a G_k-only slot: G0 contributes an exact zero
-                bool is_dom = false;
+                bool is_dom = false, is_imag = false;
                 if (j0 < g.row_ptr[i + 1] && g.col_ind[j0] == c) {
                     Key key;
                     memcpy(&key.a, &g.values[2 * j0], 8);
                     memcpy(&key.b, &g.values[2 * j0 + 1], 8);
                     is_dom = dom_on && key.a == dom_key.a && key.b == dom_key.b;
-                    if (!is_dom) vi = lookup(index, dict, g.values[2 * j0], g.values[2 * j0 + 1]);
+                    is_imag = !is_dom && imag_on && key.a == 0;
+                    if (is_imag) {
+                        auto it = iindex.find(key.b);
+                        if (it == iindex.end()) {
+                            it = iindex.emplace(key.b, (int)idict.size()).first;
+                            idict.push_back(g.values[2 * j0 + 1]);
+                        }
+                        vi = it->second;
+                        any_imag = true;
+                    } else if (!is_dom) {
+                        vi = lookup(index, dict, g.values[2 * j0], g.values[2 * j0 + 1]);
+                    }
                     ++j0;
                 }
                 if (vi < 0) { ok = false; break; }
-                const size_t slot = slot_of(sl, k, lane);
+                // entries from the diagonal on move behind the inserted zeros
+                const size_t kk = k + (imag_on && c >= i ? (size_t)prepad[i] : 0);
+                const size_t slot = slot_of(sl, kk, lane);
                 if (is_dom) {  // bit 0: the value is DevProblem::sell_dom
                     ent[slot] = 1u | ((uint32_t)(16 * c) << 16);
+                    if (imag_on) ikind[slot] = 0u;
                     continue;
                 }
                 // texture-path variants (sell_uses_tex): the value index itself
                 ent[slot] = (uint32_t)(use_tex ? vi : 16 * vi) | ((uint32_t)(16 * c) << 16);
+                if (imag_on) {
+                    ikind[slot] = is_imag ? 1u : 0u;
+                    if (is_imag) ent[slot] = (uint32_t)vi | ((uint32_t)(16 * c) << 16);
+                }
                 for (int t = 0; t < nt1; ++t) {
                     const qtm_csr* m = tds[t];
                     int ti = 0;
@@ -495,6 +549,26 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
                     if (ti < 0) { ok = false; break; }
                     tent[(size_t)t * nslot + slot] = (uint16_t)(16 * ti);
                 }
+            }
+        }
+        if (!ok) continue;
+        // the 8-byte values sit behind the complex ones (as pairs in the same
+        // array); without any the encoding is the plain one
+        const bool use_imag = imag_on && any_imag;
+        if (imag_on) {
+            if (use_imag && 16 * dict.size() + 8 * idict.size() > 65536) continue;
+            const uint32_t ibase = (uint32_t)(16 * dict.size());
+            for (size_t sidx = 0; sidx < nslot; ++sidx) {
+                if (!ikind[sidx]) continue;
+                if (use_imag) {  // bit 1 + byte offset of the double
+                    ent[sidx] = (ent[sidx] & 0xFFFF0000u) | 2u | (ibase + 8u * (ent[sidx] & 0xFFFFu));
+                } else {  // (no imaginary-only entries: every kind-1 slot is padding)
+                    ent[sidx] = 0u;
+                }
+            }
+            if (use_imag) {
+                if (idict.size() % 2) idict.push_back(0.0);
+                for (size_t q = 0; q < idict.size(); q += 2) dict.push_back(make_double2(idict[q], idict[q + 1]));
             }
         }
         if (!ok) continue;
@@ -519,7 +593,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         P.sell_td = 0;
         P.sell_td_dict_n = 0;
         P.sell_tex = 0;
-        P.sell_dom_on = dom_on ? 1 : 0;
+        P.sell_dom_on = (dom_on ? 1 : 0) | (use_imag ? 2 : 0);
         P.sell_dom = 0.0;
         if (dom_on) memcpy(&P.sell_dom, &dom_key.b, 8);
         if (use_tex) {
@@ -930,10 +1004,11 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         std::vector<const qtm_csr*> tds;
         if (var.td)
             for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
-        const bool dom_env = !(getenv("QTM_DOM") && atoi(getenv("QTM_DOM")) == 0);  // A/B: QTM_DOM=0
+        // A/B: QTM_DOM = 0 (off) / 1 (dominant value only) / 2 (8-byte imaginary values only) / 3
+        const int dom_env = getenv("QTM_DOM") ? atoi(getenv("QTM_DOM")) : 3;
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds,
                         sell_uses_tex(var.threads, var.comps, var.reg_rows, var.td != 0),
-                        dom_env && sell_uses_dom(var.threads, var.comps, var.reg_rows, var.td != 0));
+                        sell_uses_dom(var.threads, var.comps, var.reg_rows, var.td != 0) ? dom_env : 0);
     }
     if (rc == QTM_OK && p->method == 0 && !var.small) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->method == 0 && var.tm) {

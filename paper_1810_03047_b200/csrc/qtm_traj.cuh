@@ -97,6 +97,9 @@ struct DevProblem {
     // makes up most of G's stored entries (every off-diagonal of c4's Ising
     // chain is i h), its entries carry bit 0 instead of a dictionary offset
     // and take the value from this field: no dictionary load for them
+    // (sell_dom_on bit 0).  Other purely imaginary values are stored as one
+    // double behind the complex dictionary; their entries carry bit 1 and the
+    // double's byte offset (sell_dom_on bit 1): an 8-byte load.
     int sell_dom_on;
     double sell_dom;
     const int* sell_off;    // [NT/32] first entry slot of each warp (SellSlots)
@@ -414,13 +417,56 @@ __device__ __forceinline__ double2 tex_val(unsigned long long tex, uint32_t u) {
 __host__ __device__ constexpr bool sell_uses_dom(int threads, int comps, int reg_rows, bool td) {
     return QTM_SELL_DOM && comps > 1 && reg_rows > 0 && !td && !sell_uses_tex(threads, comps, reg_rows, td);
 }
-__device__ __forceinline__ double2 sell_val_dom(uint32_t dbs, uint32_t u, double dom) {
-    double2 v = make_double2(0.0, dom);
-    asm("{\n\t.reg .pred q;\n\t.reg .b32 t;\n\tand.b32 t, %3, 1;\n\tsetp.eq.u32 q, t, 0;\n\t"
-        "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
-        : "+d"(v.x), "+d"(v.y)
-        : "r"(dbs + (u & 0xFFFFu)), "r"(u));
+// MODE bit 0: entries with bit 0 take the dominant value; MODE bit 1: entries
+// with bit 1 are purely imaginary and load 8 bytes (the imaginary part) from
+// the offset in bits 3..15.  The loads are predicated per lane; lanes whose
+// predicate is off move nothing through the shared-memory pipe.
+template <int MODE>
+__device__ __forceinline__ double2 sell_val_flag(uint32_t dbs, uint32_t u, double dom) {
+    double2 v = make_double2(0.0, (MODE & 1) ? dom : 0.0);
+    const uint32_t a = dbs + (u & 0xFFF8u);
+    if constexpr (MODE == 1) {
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 t;\n\tand.b32 t, %3, 1;\n\tsetp.eq.u32 q, t, 0;\n\t"
+            "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t}"
+            : "+d"(v.x), "+d"(v.y) : "r"(a), "r"(u));
+    } else if constexpr (MODE == 2) {
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 t;\n\tand.b32 t, %3, 2;\n\tsetp.eq.u32 q, t, 0;\n\t"
+            "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t@!q ld.shared.f64 %1, [%2];\n\t}"
+            : "+d"(v.x), "+d"(v.y) : "r"(a), "r"(u));
+    } else {
+        asm("{\n\t.reg .pred q, r;\n\t.reg .b32 t;\n\tand.b32 t, %3, 3;\n\tsetp.eq.u32 q, t, 0;\n\t"
+            "and.b32 t, %3, 2;\n\tsetp.ne.u32 r, t, 0;\n\t"
+            "@q ld.shared.v2.f64 {%0, %1}, [%2];\n\t@r ld.shared.f64 %1, [%2];\n\t}"
+            : "+d"(v.x), "+d"(v.y) : "r"(a), "r"(u));
+    }
     return v;
+}
+// the pipelined column loop of the wide variants with flagged entries (one
+// copy per MODE, chosen per problem: problems without such entries keep the
+// plain loop below and pay nothing)
+template <int E, int MODE>
+__device__ __forceinline__ void sell_cols_flag(const uint32_t* __restrict__ p, const char* db, const char* xb,
+                                               int width, double dom, double (&sr)[E], double (&si)[E]) {
+    using S = SellSlots<E>;
+    if (width <= 0) return;
+    const uint32_t dbs = (uint32_t)__cvta_generic_to_shared(db);
+    uint32_t u[E];
+    S::load(p, u);
+    QTM_SPMV_UNROLL_PRAGMA
+    for (int k = 1; k < width; ++k) {
+        double2 v[E], xv[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            v[e] = sell_val_flag<MODE>(dbs, u[e], dom);
+            xv[e] = sell_x(xb, u[e]);
+        }
+        p += 32 * E;
+        S::load(p, u);
+#pragma unroll
+        for (int e = 0; e < E; ++e) cmac(sr[e], si[e], v[e], xv[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) cmac(sr[e], si[e], sell_val_flag<MODE>(dbs, u[e], dom), sell_x(xb, u[e]));
 }
 template <int NT, int E, int PF, bool TEX = false, bool DOM = false>
 __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
@@ -483,28 +529,9 @@ __device__ __forceinline__ void sell_spmv(const uint32_t* __restrict__ ent,
             cmac(sr[0], si[0], v, xv);
         }
     } else if (DOM && dom_on) {
-        // the same pipelined loop with the dominant value's entries served
-        // from `dom` (a separate copy, so problems without one pay nothing)
-        if (width > 0) {
-            const uint32_t dbs = (uint32_t)__cvta_generic_to_shared(db);
-            uint32_t u[E];
-            S::load(p, u);
-            QTM_SPMV_UNROLL_PRAGMA
-            for (int k = 1; k < width; ++k) {
-                double2 v[E], xv[E];
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    v[e] = sell_val_dom(dbs, u[e], dom);
-                    xv[e] = sell_x(xb, u[e]);
-                }
-                p += 32 * E;
-                S::load(p, u);
-#pragma unroll
-                for (int e = 0; e < E; ++e) cmac(sr[e], si[e], v[e], xv[e]);
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) cmac(sr[e], si[e], sell_val_dom(dbs, u[e], dom), sell_x(xb, u[e]));
-        }
+        if (dom_on == 1) sell_cols_flag<E, 1>(p, db, xb, width, dom, sr, si);
+        else if (dom_on == 2) sell_cols_flag<E, 2>(p, db, xb, width, dom, sr, si);
+        else sell_cols_flag<E, 3>(p, db, xb, width, dom, sr, si);
     } else if (width > 0) {
         uint32_t u[E];
         S::load(p, u);

@@ -23,6 +23,7 @@ and one all-reduce of the per-point sums.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass
 
@@ -137,16 +138,48 @@ def bytes_model(stats_total: dict, packed: PackedProblem) -> float:
     return float(16 * d * (2 * (stats_total["sum_q"] + att) + 2 * att))
 
 
-def smem_model(stats_total: dict, packed: PackedProblem) -> float:
+def spmv_value_bytes(packed: PackedProblem, shape=None) -> int:
+    """Dictionary-value bytes one staged SpMV loads per thread-row set (summed
+    over G's stored entries).  16 per entry in general.  On the wide variants
+    (several rows per thread, pipelined SpMV; `sell_uses_dom` in
+    csrc/qtm_traj.cuh, rule restated from `build_sell` in csrc/qtm_capi.cu)
+    the entries of a dominant purely imaginary value (at least half of the
+    entries) load nothing, and the other purely imaginary values (if at least
+    a quarter of the entries) load 8 bytes."""
+    nnz = packed.g.nnz
+    wide = (shape is not None and shape[1] > 1 and shape[2] > 0 and not packed.td
+            and os.environ.get("QTM_DOM", "3") != "0")
+    if not wide or nnz == 0:
+        return 16 * nnz
+    mode = int(os.environ.get("QTM_DOM", "3"))
+    vals = np.asarray(packed.g.values).view(np.float64).reshape(-1, 2)
+    imag = vals[:, 0].view(np.uint64) == 0  # re is +0.0 bit for bit
+    n_dom = 0
+    if imag.any():
+        _, counts = np.unique(vals[imag, 1].view(np.uint64), return_counts=True)
+        best = int(counts.max())
+        if (mode & 1) and 2 * best >= nnz:
+            n_dom = best
+    n_other = int(imag.sum()) - n_dom
+    if not (mode & 2) or 4 * n_other < nnz:
+        n_other = 0
+    return 16 * (nnz - n_dom - n_other) + 8 * n_other
+
+
+def smem_model(stats_total: dict, packed: PackedProblem, shape=None) -> float:
     """Shared-memory bytes the Adams trajectory kernel moves by construction
     (DESIGN.md §3): per corrector iteration the staged-operator SpMV reads an
-    entry word, a 16-byte dictionary value and a 16-byte gathered x per
-    nonzero (36 nnz), and the update reads the iterate and the weight and
-    writes the next iterate (40 d); per attempt the predicted z0 is published
-    once (16 d).  Reductions, row 0 of the TMEM variant and recording come on
-    top, so the measured wavefronts (ncu) are higher."""
+    entry word and a 16-byte gathered x per nonzero (20 nnz) plus the
+    dictionary values (`spmv_value_bytes`: 16 per nonzero in general, fewer
+    on the wide variants when G's off-diagonals are purely imaginary), and
+    the update reads the iterate and the weight and writes the next iterate
+    (40 d); per attempt the predicted z0 is published once (16 d).
+    Reductions, row 0 of the TMEM variant and recording come on top, so the
+    measured wavefronts (ncu) are higher.  `shape` = the kernel variant's
+    (threads, components, register rows)."""
     d, nnz = packed.dim, packed.g.nnz
-    return float(stats_total["corr_iters"] * (36 * nnz + 40 * d) + stats_total["attempts"] * 16 * d)
+    per_spmv = 20 * nnz + spmv_value_bytes(packed, shape)
+    return float(stats_total["corr_iters"] * (per_spmv + 40 * d) + stats_total["attempts"] * 16 * d)
 
 
 @dataclass
