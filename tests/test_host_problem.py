@@ -173,3 +173,27 @@ def test_average_and_standard_error():
     np.testing.assert_allclose(out.values, 1.6)
     r = TrajectoryResult(t, np.full((1, 3), 0.5), 4, sumsq=np.full((1, 3), 2.0))
     np.testing.assert_allclose(r.standard_error(), np.sqrt((0.5 - 0.25) * 4 / 3 / 4))
+
+
+def test_spmv_value_bytes_follow_the_staging_rule():
+    """engine.spmv_value_bytes restates build_sell's rule (csrc/qtm_capi.cu): on
+    the wide variants a dominant purely imaginary value (>= half the entries)
+    loads nothing, other purely imaginary values (>= a quarter) load 8 bytes,
+    everything else 16; the narrow variants load 16 per entry."""
+    from paper_1810_03047_b200 import configs
+    from paper_1810_03047_b200.engine import smem_model, spmv_value_bytes
+    from paper_1810_03047_b200.packing import pack_problem
+
+    c4 = pack_problem(configs.build("c4"))
+    c5 = pack_problem(configs.build("c5"))
+    wide, narrow = (256, 4, 8), (32, 1, 0)
+    # c4: 10 240 off-diagonals are i*h (dominant), 1 024 diagonals stay complex
+    assert c4.g.nnz == 11264
+    assert spmv_value_bytes(c4, wide) == 16 * 1024
+    assert spmv_value_bytes(c4, narrow) == 16 * c4.g.nnz
+    assert spmv_value_bytes(c4, None) == 16 * c4.g.nnz
+    # c5: no dominant value; 3 422 purely imaginary off-diagonals at 8 bytes, 899 diagonals at 16
+    assert spmv_value_bytes(c5, wide) == 8 * 3422 + 16 * 899
+    st = {"corr_iters": 10, "attempts": 5}
+    assert smem_model(st, c4, wide) < smem_model(st, c4, narrow)
+    assert smem_model(st, c4, narrow) == 10 * (36 * c4.g.nnz + 40 * 1024) + 5 * 16 * 1024

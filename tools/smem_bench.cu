@@ -6,6 +6,8 @@
 //   4. LDS.64 / LDS.32, distinct addresses
 //   5. tex1Dfetch<int4> from a 1 KB table, 8 distinct addresses per warp
 //   6. 1 + 5 interleaved: do the texture fetches ride on top of the LDS traffic?
+//   7. LDS.64 values (purely imaginary entries), alone and beside the gather; per-lane
+//      mixes of predicated LDS.128 / LDS.64 values; a dominant value held in registers
 // Prints cycles per warp instruction per SM at 16 resident warps per SM.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o smem_bench tools/smem_bench.cu && ./smem_bench
 #include <cstdio>
@@ -85,13 +87,6 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
                 const int2* const h = reinterpret_cast<const int2*>(buf);
                 const int2 a = h[((MODE == 12 ? 5 : ((lane * 7) & 7)) + 8 * u + o2) & 63];
                 acc.x ^= a.x; acc.y ^= a.y;
-            } else if (MODE >= 14 && MODE <= 17) {
-                // predicated LDS.128, 8-entry dictionary addresses; active lanes:
-                // 14: popcount(lane) == 2 (10 lanes, in every quarter-warp)
-                // 15: lanes 0..7 (one quarter-warp)   16: lane 0   17: none
-                const int on = MODE == 14 ? (__popc(lane) == 2) : MODE == 15 ? (lane < 8) : MODE == 16 ? (lane == 0) : (acc.w == 0x7ffffff1);
-                const int4 w = lds128_if(&buf[(((lane * 7) & 7) + 8 * u + o2) & 63], on, make_int4(1, 2, 3, 4));
-                acc.x ^= w.x; acc.y ^= w.y; acc.z ^= w.z; acc.w ^= w.w;
             } else if (MODE == 18 || MODE == 19) {
                 // gather + LDS.64 value (one address / 8 distinct)
                 const int4 v = buf[(idx + 32 * u + o1) & 2047];
@@ -126,56 +121,6 @@ __global__ void __launch_bounds__(512, 1) k(cudaTextureObject_t tex, long long* 
     long long t1 = clock64();
     if (tid == 0) out[blockIdx.x] = t1 - t0;
     if (acc.x == 0x7fffffff) sink[0] = acc;
-}
-
-// Predicated loads, pipe-bound form: the address and the predicate are set up
-// outside the timed loop and each step is one predicated load plus one XOR, so
-// the issue slots (16 warps per SM: 4 instructions per SM-cycle) stay far from
-// binding.  WIDTH = 16 / 8 bytes; PAT = which lanes are on:
-//   0 all, 1 popcount(lane) == 2 (10 lanes, every quarter-warp), 2 lanes 0..7,
-//   3 lane 0, 4 none, 5 lanes 0..15, 6 even lanes
-template <int WIDTH, int PAT, bool SAME>
-__global__ void __launch_bounds__(512, 1) kp(long long* out, int4* sink) {
-    __shared__ int4 buf[2048];
-    const int tid = threadIdx.x, lane = tid & 31;
-    for (int i = tid; i < 2048; i += blockDim.x) buf[i] = make_int4(i, i + 1, i + 2, i + 3);
-    __syncthreads();
-    const int on = PAT == 0 ? 1 : PAT == 1 ? (__popc(lane) == 2) : PAT == 2 ? (lane < 8) : PAT == 3 ? (lane == 0)
-                 : PAT == 4 ? (tid == 4096) : PAT == 5 ? (lane < 16) : ((lane & 1) == 0);
-    const unsigned a0 = (unsigned)__cvta_generic_to_shared(buf) + (SAME ? 80u : (unsigned)(((lane * 7) & 7) * 16));
-    int acc = 0;
-    long long t0 = clock64();
-    for (int it = 0; it < ITERS; ++it) {
-        const unsigned a = a0 + ((unsigned)(acc & 32) << 4);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            int x = 1, y = 2, z = 3, w = 4;
-            if (WIDTH == 16)
-                asm volatile("{ .reg .pred q; setp.ne.s32 q, %5, 0; @q ld.shared.v4.s32 {%0,%1,%2,%3}, [%4+%6]; }"
-                             : "+r"(x), "+r"(y), "+r"(z), "+r"(w) : "r"(a), "r"(on), "n"(0));
-            else
-                asm volatile("{ .reg .pred q; setp.ne.s32 q, %3, 0; @q ld.shared.v2.s32 {%0,%1}, [%2+%4]; }"
-                             : "+r"(x), "+r"(y) : "r"(a), "r"(on), "n"(0));
-            acc ^= WIDTH == 16 ? (x ^ y ^ z ^ w) : (x ^ y);  // every loaded word consumed (or ptxas narrows the load)
-        }
-    }
-    long long t1 = clock64();
-    if (tid == 0) out[blockIdx.x] = t1 - t0;
-    if (acc == 0x7fffffff) sink[0] = make_int4(acc, 0, 0, 0);
-}
-template <int WIDTH, int PAT, bool SAME>
-static void runp(const char* name, long long* d_out, int4* d_sink, int sms) {
-    kp<WIDTH, PAT, SAME><<<sms, 512>>>(d_out, d_sink);
-    cudaDeviceSynchronize();
-    kp<WIDTH, PAT, SAME><<<sms, 512>>>(d_out, d_sink);
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
-    long long h[256];
-    cudaMemcpy(h, d_out, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
-    double avg = 0;
-    for (int i = 0; i < sms; ++i) avg += (double)h[i];
-    avg /= sms;
-    printf("%-58s %8.2f SM-cycles per warp step (16 warps/SM)\n", name, avg / ((double)ITERS * UNR * 16));
 }
 
 template <int MODE>
@@ -226,30 +171,12 @@ int main() {
     run<11>("LDS.128 distinct + LDS.128 one address", tex, d_out, d_sink, sms);
     run<12>("LDS.64, one address for the warp", tex, d_out, d_sink, sms);
     run<13>("LDS.64, 8 distinct addresses", tex, d_out, d_sink, sms);
-    run<14>("@p LDS.128 8-address, 10 lanes on (every quarter-warp)", tex, d_out, d_sink, sms);
-    run<15>("@p LDS.128 8-address, lanes 0..7 on", tex, d_out, d_sink, sms);
-    run<16>("@p LDS.128 8-address, lane 0 on", tex, d_out, d_sink, sms);
-    run<17>("@p LDS.128 8-address, no lane on", tex, d_out, d_sink, sms);
     run<18>("LDS.128 distinct + LDS.64 one address", tex, d_out, d_sink, sms);
     run<19>("LDS.128 distinct + LDS.64 8-address", tex, d_out, d_sink, sms);
     run<20>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, 10 lanes complex", tex, d_out, d_sink, sms);
     run<21>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, lanes 0..7 complex", tex, d_out, d_sink, sms);
     run<22>("LDS.128 distinct + @p LDS.128 / @!p LDS.64, no lane complex", tex, d_out, d_sink, sms);
     run<23>("LDS.128 distinct + @p LDS.128 10 lanes (dominant value in registers)", tex, d_out, d_sink, sms);
-    runp<16, 0, false>("@p LDS.128 8-address, all lanes on [pipe-bound form]", d_out, d_sink, sms);
-    runp<16, 1, false>("@p LDS.128 8-address, 10 lanes on, every quarter", d_out, d_sink, sms);
-    runp<16, 5, false>("@p LDS.128 8-address, lanes 0..15 on", d_out, d_sink, sms);
-    runp<16, 6, false>("@p LDS.128 8-address, even lanes on", d_out, d_sink, sms);
-    runp<16, 2, false>("@p LDS.128 8-address, lanes 0..7 on", d_out, d_sink, sms);
-    runp<16, 3, false>("@p LDS.128 8-address, lane 0 on", d_out, d_sink, sms);
-    runp<16, 4, false>("@p LDS.128 8-address, no lane on", d_out, d_sink, sms);
-    runp<16, 0, true>("@p LDS.128 one address, all lanes on", d_out, d_sink, sms);
-    runp<16, 1, true>("@p LDS.128 one address, 10 lanes on", d_out, d_sink, sms);
-    runp<8, 0, false>("@p LDS.64 8-address, all lanes on", d_out, d_sink, sms);
-    runp<8, 1, false>("@p LDS.64 8-address, 10 lanes on, every quarter", d_out, d_sink, sms);
-    runp<8, 5, false>("@p LDS.64 8-address, lanes 0..15 on", d_out, d_sink, sms);
-    runp<8, 4, false>("@p LDS.64 8-address, no lane on", d_out, d_sink, sms);
-    runp<8, 0, true>("@p LDS.64 one address, all lanes on", d_out, d_sink, sms);
     run<5>("tex1Dfetch<int4>, 8 distinct addresses", tex, d_out, d_sink, sms);
     run<6>("LDS.128 distinct + tex1Dfetch<int4> (x + value via TEX)", tex, d_out, d_sink, sms);
     return 0;
