@@ -113,6 +113,15 @@ SMALL_VARIANTS = [
     (4, 1, 4),     # 42  automatic for 2 < d <= 4
 ]
 
+# variants added after the small ones (so the ids above stay what tests, docs
+# and profiles call them): same tuple format as VARIANTS
+LATE_VARIANTS = [
+    # the TMEM variant with the time-dependent terms compiled in: fits two CTAs
+    # per SM when the staged term needs no per-slot tables (sell_spmv_tdd:
+    # c4td's modulated field is one value), else one
+    (256, 4, 8, 2, 0, True, True),       # 43
+]
+
 SOURCES = ["qtm_traj.cuh", "qtm_bdf.cuh", "qtm_rng.cuh", "qtm_tmem.cuh", "qtm_small.cuh", "qtm_capi.cu"]
 
 
@@ -135,28 +144,30 @@ def generate() -> list[str]:
     files = []
     decls = []
     rows = []
-    for i, row in enumerate(VARIANTS):
-        nt, e, rr, mb, auto = row[:5]
-        td = "true" if len(row) > 5 and row[5] else "false"
-        tmem = "true" if len(row) > 6 and row[6] else "false"
-        name = f"variant_{i}.cu"
-        body = f"""// generated by build.py -- kernel variant {i}
+    def emit(i, row):
+            nt, e, rr, mb, auto = row[:5]
+            td = "true" if len(row) > 5 and row[5] else "false"
+            tmem = "true" if len(row) > 6 and row[6] else "false"
+            name = f"variant_{i}.cu"
+            body = f"""// generated by build.py -- kernel variant {i}
 #include "../qtm_traj.cuh"
 namespace qtm {{
 template __global__ void traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>(const __grid_constant__ DevProblem,
-                                                                 const __grid_constant__ RunParams);
+                                                                     const __grid_constant__ RunParams);
 VariantDesc variant_{i}() {{
     return VariantDesc{{{nt}, {e}, {rr}, {mb}, {auto}, {1 if td == "true" else 0},
-                       TrajKernel<{nt}, {e}, {rr}, {tmem}>::smem_bytes(),
-                       reinterpret_cast<const void*>(traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>),
-                       {1 if tmem == "true" else 0}, 0, 0}};
+                           TrajKernel<{nt}, {e}, {rr}, {tmem}>::smem_bytes(),
+                           reinterpret_cast<const void*>(traj_kernel<{nt}, {e}, {rr}, {mb}, {td}, {tmem}>),
+                           {1 if tmem == "true" else 0}, 0, 0}};
 }}
 }}  // namespace qtm
 """
-        _write_if_changed(os.path.join(GEN, name), body)
-        files.append(os.path.join(GEN, name))
-        decls.append(f"VariantDesc variant_{i}();")
-        rows.append(f"        variant_{i}(),")
+            _write_if_changed(os.path.join(GEN, name), body)
+            files.append(os.path.join(GEN, name))
+            decls.append(f"VariantDesc variant_{i}();")
+            rows.append(f"        variant_{i}(),")
+    for i, row in enumerate(VARIANTS):
+        emit(i, row)
     for j, (dmax, lanes, auto) in enumerate(SMALL_VARIANTS):
         i = len(VARIANTS) + j
         name = f"variant_{i}.cu"
@@ -175,6 +186,8 @@ VariantDesc variant_{i}() {{
         files.append(os.path.join(GEN, name))
         decls.append(f"VariantDesc variant_{i}();")
         rows.append(f"        variant_{i}(),")
+    for j, row in enumerate(LATE_VARIANTS):
+        emit(len(VARIANTS) + len(SMALL_VARIANTS) + j, row)
     table = ("// generated by build.py\nnamespace qtm {\n" + "\n".join(decls) + "\n}  // namespace qtm\n"
              "static const std::vector<qtm::VariantDesc>& qtm_variant_table() {\n"
              "    using namespace qtm;\n    static const std::vector<VariantDesc> t = {\n"
@@ -190,6 +203,7 @@ def _stamp(paths) -> str:
     h.update(" ".join(NVCC_FLAGS).encode())
     h.update(repr(VARIANTS).encode())
     h.update(repr(SMALL_VARIANTS).encode())
+    h.update(repr(LATE_VARIANTS).encode())
     return h.hexdigest()
 
 

@@ -379,7 +379,7 @@ int upload_csr(qtm_problem* p, const qtm_csr& m, int64_t n, DevCsr* out, const c
 // L2 (row_dot).
 int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, size_t fixed_smem,
                size_t smem_cap, bool* staged, const std::vector<const qtm_csr*>& tds = {},
-               bool use_tex = false, int use_dom = 0) {
+               bool use_tex = false, int use_dom = 0, bool use_tdd = false) {
     *staged = false;
     const int dp = nt * ncomp;
     const int nslices = dp / 32, nw = nt / 32;
@@ -443,7 +443,17 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         bool dom_on = false;
         Key dom_key{0, 0};
         int64_t n_imag_other = 0;  // purely imaginary entries besides the dominant value
-        if (use_dom && !use_tex && nt1 == 0) {
+        // sell_uses_tdd variants, one staged term whose stored entries all hold
+        // one value: no per-slot table, bit 2 of the G0 entry marks G_1's
+        // pattern (sell_spmv_tdd), and G0's dominant value rides on bit 0
+        bool tdd = false;
+        if (use_tdd && nt1 == 1 && !use_tex && tds[0]->row_ptr[n] > 0) {
+            const qtm_csr* m = tds[0];
+            tdd = true;
+            for (int64_t j = 1; j < m->row_ptr[n] && tdd; ++j)
+                tdd = memcmp(&m->values[2 * j], &m->values[0], 16) == 0;
+        }
+        if ((use_dom && !use_tex && nt1 == 0) || tdd) {
             std::map<Key, int64_t> freq;
             const int64_t nnz = g.row_ptr[n];
             int64_t n_imag = 0;
@@ -456,12 +466,12 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             int64_t best = 0;
             for (const auto& kv : freq)
                 if (kv.second > best) { best = kv.second; dom_key = kv.first; }
-            dom_on = (use_dom & 1) && nnz > 0 && 2 * best >= nnz;
+            dom_on = ((use_dom & 1) || tdd) && nnz > 0 && 2 * best >= nnz;
             n_imag_other = n_imag - (dom_on ? best : 0);
             // 8-byte values only where they are a sizeable share of the entries
             // (c5: 79 %); a handful (c4: one diagonal entry) stays complex, so the
             // kernel runs the loop without the second predicated load
-            if (4 * n_imag_other < nnz) n_imag_other = 0;
+            if (4 * n_imag_other < nnz || tdd) n_imag_other = 0;
         }
         std::vector<uint32_t> ent(std::max(total, 1), 0u);  // padding: x[0] * dict[0] (= 0)
         const size_t nslot = (size_t)std::max(total, 1);
@@ -528,6 +538,13 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
                 // entries from the diagonal on move behind the inserted zeros
                 const size_t kk = k + (imag_on && c >= i ? (size_t)prepad[i] : 0);
                 const size_t slot = slot_of(sl, kk, lane);
+                if (tdd) {  // bit 2: G_1 has an entry in this slot (its one value: sell_td_dom)
+                    const qtm_csr* m = tds[0];
+                    const bool has1 = jt[0] < m->row_ptr[i + 1] && m->col_ind[jt[0]] == c;
+                    if (has1) ++jt[0];
+                    ent[slot] = (is_dom ? 1u : (uint32_t)(16 * vi)) | (has1 ? 4u : 0u) | ((uint32_t)(16 * c) << 16);
+                    continue;
+                }
                 if (is_dom) {  // bit 0: the value is DevProblem::sell_dom
                     ent[slot] = 1u | ((uint32_t)(16 * c) << 16);
                     if (imag_on) ikind[slot] = 0u;
@@ -573,7 +590,7 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
         }
         if (!ok) continue;
         size_t bytes = sizeof(double2) * dict.size() + sizeof(uint32_t) * ent.size();
-        if (nt1) bytes += sizeof(double2) * tdict.size() + sizeof(uint16_t) * tent.size();
+        if (nt1 && !tdd) bytes += sizeof(double2) * tdict.size() + sizeof(uint16_t) * tent.size();
         if (fixed_smem + bytes > smem_cap) continue;
         uint32_t* d_ent = nullptr;
         double2* d_dict = nullptr;
@@ -609,7 +626,15 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             P.sell_tex = (unsigned long long)tex;
             p->sell_tex = tex;
         }
-        if (nt1) {
+        P.sell_td_dom_on = 0;
+        P.sell_td_dom = make_double2(0.0, 0.0);
+        if (tdd) {
+            P.sell_td = 1;
+            P.sell_td_dict = nullptr;
+            P.sell_td_ent = nullptr;
+            P.sell_td_dom_on = 1;
+            memcpy(&P.sell_td_dom, &tds[0]->values[0], 16);
+        } else if (nt1) {
             double2* d_tdict = nullptr;
             uint16_t* d_tent = nullptr;
             CUDA_TRY(upload(p, &d_tdict, tdict.data(), tdict.size()));
@@ -841,6 +866,25 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
     if (!d->l_table || !d->tau1 || !d->tau2 || !d->tau3) return set_error(QTM_ERR_ARGS, "Adams tables missing");
     // (BDF runs its own kernel, qtm_bdf.cuh; the Adams variant slot is unused)
     int variant = d->method == 1 ? 0 : (d->variant >= 0 ? d->variant : auto_variant(d->dim, d->n_td > 0));
+    // one time-dependent term whose entries all hold one value needs no
+    // per-slot tables (sell_spmv_tdd), so a 512 < d <= 1024 trajectory fits
+    // the TMEM variant's two CTAs per SM: the automatic choice then
+    // (c4td 249 -> 201 ms per 4 096 trajectories against the register variant)
+    if (d->method == 0 && d->variant < 0 && d->n_td == 1 && d->dim > 512 && d->dim <= 1024 &&
+        d->td[0].row_ptr && d->td[0].values && d->td[0].row_ptr[d->dim] > 0 &&
+        ((getenv("QTM_DOM") ? atoi(getenv("QTM_DOM")) : 7) & 4)) {
+        const qtm_csr& m = d->td[0];
+        bool one = true;
+        for (int64_t j = 1; j < m.row_ptr[d->dim] && one; ++j)
+            one = memcmp(&m.values[2 * j], &m.values[0], 16) == 0;
+        if (one)
+            for (int i = 0; i < (int)variants().size(); ++i)
+                if (variants()[i].td && variants()[i].tm && !variants()[i].small &&
+                    (int64_t)variants()[i].threads * variants()[i].comps >= d->dim) {
+                    variant = i;
+                    break;
+                }
+    }
     if (variant < 0 || variant >= (int)variants().size())
         return set_error(QTM_ERR_UNSUPPORTED, "no kernel variant for this dimension");
     const Variant& var = variants()[variant];
@@ -1004,11 +1048,13 @@ int qtm_problem_create(const qtm_problem_desc* d, qtm_problem** out) {
         std::vector<const qtm_csr*> tds;
         if (var.td)
             for (int k = 0; k < d->n_td; ++k) tds.push_back(&d->td[k]);
-        // A/B: QTM_DOM = 0 (off) / 1 (dominant value only) / 2 (8-byte imaginary values only) / 3
-        const int dom_env = getenv("QTM_DOM") ? atoi(getenv("QTM_DOM")) : 3;
+        // A/B: QTM_DOM bits: 1 dominant value, 2 8-byte imaginary values, 4 single-valued
+        // time-dependent term without tables (TD variants); default all
+        const int dom_env = getenv("QTM_DOM") ? atoi(getenv("QTM_DOM")) : 7;
         rc = build_sell(p, d->generator, d->dim, var.threads, var.comps, var.smem, dyn_cap, &staged, tds,
                         sell_uses_tex(var.threads, var.comps, var.reg_rows, var.td != 0),
-                        sell_uses_dom(var.threads, var.comps, var.reg_rows, var.td != 0) ? dom_env : 0);
+                        sell_uses_dom(var.threads, var.comps, var.reg_rows, var.td != 0) ? dom_env : 0,
+                        (dom_env & 4) && sell_uses_tdd(var.comps, var.reg_rows, var.td != 0));
     }
     if (rc == QTM_OK && p->method == 0 && !var.small) rc = build_expect_diag(p, d, var.threads * var.comps);
     if (rc == QTM_OK && p->method == 0 && var.tm) {

@@ -111,6 +111,12 @@ struct DevProblem {
     int sell_td, sell_td_dict_n;
     const double2* sell_td_dict;
     const uint16_t* sell_td_ent;
+    // a single staged term whose stored entries all hold ONE value (c4td: the
+    // modulated transverse field): no per-slot table at all -- bit 2 of the
+    // G0 entry says "G_1 has an entry here", its value is sell_td_dom, and
+    // G0's dominant value rides on bit 0 as in the time-independent kernels
+    int sell_td_dom_on;
+    double2 sell_td_dom;
     // observables that are diagonal in the basis (number operators, sigma_z):
     // bit k of e_diag_mask set => dense values at e_diag[k * DP + i]
     unsigned e_diag_mask;
@@ -417,6 +423,10 @@ __device__ __forceinline__ double2 tex_val(unsigned long long tex, uint32_t u) {
 __host__ __device__ constexpr bool sell_uses_dom(int threads, int comps, int reg_rows, bool td) {
     return QTM_SELL_DOM && comps > 1 && reg_rows > 0 && !td && !sell_uses_tex(threads, comps, reg_rows, td);
 }
+// the TD variants that take the single-valued-term form (sell_spmv_tdd)
+__host__ __device__ constexpr bool sell_uses_tdd(int comps, int reg_rows, bool td) {
+    return QTM_SELL_DOM && td && comps > 1 && reg_rows > 0;
+}
 // MODE bit 0: entries with bit 0 take the dominant value; MODE bit 1: entries
 // with bit 1 are purely imaginary and load 8 bytes (the imaginary part) from
 // the offset in bits 3..15.  The loads are predicated per lane; lanes whose
@@ -583,6 +593,44 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
         for (int e = 0; e < E; ++e) {
             const double2 v = sell_val(db, u[e]);
             const double2 w = *reinterpret_cast<const double2*>(tb + tu[e]);
+            const double2 xv = sell_x(xb, u[e]);
+            cmac(sr[e], si[e], v, xv);
+            cmac(tr[e], ti[e], w, xv);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        out0[e] = make_double2(sr[e], si[e]);
+        out1[e] = make_double2(tr[e], ti[e]);
+    }
+}
+
+// The same two products when G_1's stored entries all hold one value
+// (DevProblem::sell_td_dom_on): G_1's value per slot is `tdom` where bit 2 of
+// the entry is set and an exact zero elsewhere -- the bits sell_spmv_td reads
+// from its tables -- and G0's dominant value comes from `dom` (bit 0).  Two
+// shared-memory loads per slot (entry, gathered x) plus the diagonal's value
+// instead of five.
+template <int NT, int E>
+__device__ __forceinline__ void sell_spmv_tdd(const uint32_t* __restrict__ ent, const double2* __restrict__ dict,
+                                              int woff, int width, const double2* __restrict__ x,
+                                              double2 (&out0)[E], double2 (&out1)[E], double dom, double2 tdom) {
+    using S = SellSlots<E>;
+    const int lane = threadIdx.x & 31;
+    const char* const xb = reinterpret_cast<const char*>(x);
+    const uint32_t dbs = (uint32_t)__cvta_generic_to_shared(dict);
+    double sr[E], si[E], tr[E], ti[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; tr[e] = 0.0; ti[e] = 0.0; }
+    const uint32_t* p = ent + woff + lane * S::V;
+    for (int k = 0; k < width; ++k) {
+        uint32_t u[E];
+        S::load(p, u);
+        p += 32 * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double2 v = sell_val_flag<1>(dbs, u[e], dom);
+            const double2 w = (u[e] & 4u) ? tdom : make_double2(0.0, 0.0);
             const double2 xv = sell_x(xb, u[e]);
             cmac(sr[e], si[e], v, xv);
             cmac(tr[e], ti[e], w, xv);
@@ -1464,7 +1512,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
-        if (TD && P.sell_td) {
+        if (TD && P.sell_td && !P.sell_td_dom_on) {
             for (int i = tid; i < P.sell_td_dict_n; i += NT) s_tdict[i] = P.sell_td_dict[i];
             for (int i = tid; i < P.sell_td * P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
         }
@@ -1481,7 +1529,10 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
         if constexpr (TD) {                                                  \
             if (P.sell_td == 1) {                                            \
                 double2 g__[E];                                              \
-                sell_spmv_td<NT, E>(s_ent, s_dict, s_tent, s_tdict, goff, gwidth, (xs), f, g__); \
+                if (P.sell_td_dom_on)                                        \
+                    sell_spmv_tdd<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f, g__, P.sell_dom, P.sell_td_dom); \
+                else                                                         \
+                    sell_spmv_td<NT, E>(s_ent, s_dict, s_tent, s_tdict, goff, gwidth, (xs), f, g__); \
                 const double c__ = td_coef(P, 0, (tt));                      \
                 _Pragma("unroll") for (int e = 0; e < E; ++e)                \
                     f[e] = make_double2(f[e].x + c__ * g__[e].x, f[e].y + c__ * g__[e].y); \

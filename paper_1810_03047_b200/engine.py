@@ -148,10 +148,10 @@ def spmv_value_bytes(packed: PackedProblem, shape=None) -> int:
     a quarter of the entries) load 8 bytes."""
     nnz = packed.g.nnz
     wide = (shape is not None and shape[1] > 1 and shape[2] > 0 and not packed.td
-            and os.environ.get("QTM_DOM", "3") != "0")
+            and os.environ.get("QTM_DOM", "7") != "0")
     if not wide or nnz == 0:
         return 16 * nnz
-    mode = int(os.environ.get("QTM_DOM", "3"))
+    mode = int(os.environ.get("QTM_DOM", "7"))
     vals = np.asarray(packed.g.values).view(np.float64).reshape(-1, 2)
     imag = vals[:, 0].view(np.uint64) == 0  # re is +0.0 bit for bit
     n_dom = 0

@@ -66,15 +66,19 @@ def test_td_run_gpu_and_variant_guard(oracle_lib):
         DeviceProblem(g.problem, variant=plain)
 
 
-@pytest.mark.parametrize("variant", [-1, 34, 36])
+@pytest.mark.parametrize("variant", [-1, 34, 36, 43])
 def test_td_c4td_variants_match_oracle(variant, oracle_lib):
-    """c4td (bench workload): the automatic TD variant, the former default
-    (512, 2, 8) and the (256, 4, 8) shape the autotune picks, vs the oracle."""
+    """c4td (bench workload): the automatic TD variant (the TMEM twin, 43: the
+    modulated field is a single-valued term, so two CTAs fit an SM), the former
+    defaults (512, 2, 8) and (256, 4, 8) in registers, vs the oracle."""
     from paper_1810_03047_b200 import configs
     assert native.variant_time_dependent(36) and native.variant_time_dependent(37)
+    assert native.variant_time_dependent(43) and native.variant_tmem_rows(43) > 0
     pk = pack_problem(configs.build("c4td"))
     n = 48
     with DeviceProblem(pk, variant=variant) as dp:
+        if variant == -1:
+            assert dp.layout()["variant"] == 43 and dp.max_resident() >= 2 * 132  # two CTAs per SM
         out = dp.run(goldens.SEED, 0, n, max_jumps=MAXJ)
     ref = oracle_lib.run(pk, goldens.SEED, 0, n, max_jumps=MAXJ)
     assert out.rc == ref["rc"]
