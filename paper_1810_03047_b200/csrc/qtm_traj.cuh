@@ -605,6 +605,9 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
     }
 }
 
+#ifndef QTM_TDD_PF
+#define QTM_TDD_PF 0
+#endif
 // The same two products when G_1's stored entries all hold one value
 // (DevProblem::sell_td_dom_on): G_1's value per slot is `tdom` where bit 2 of
 // the entry is set and an exact zero elsewhere -- the bits sell_spmv_td reads
@@ -623,6 +626,34 @@ __device__ __forceinline__ void sell_spmv_tdd(const uint32_t* __restrict__ ent, 
 #pragma unroll
     for (int e = 0; e < E; ++e) { sr[e] = 0.0; si[e] = 0.0; tr[e] = 0.0; ti[e] = 0.0; }
     const uint32_t* p = ent + woff + lane * S::V;
+#if QTM_TDD_PF
+    // the entries of column k+1 loaded while column k is multiplied (as the
+    // time-independent wide loop does)
+    if (width > 0) {
+        uint32_t u[E];
+        S::load(p, u);
+        for (int k = 1; k <= width; ++k) {
+            double2 v[E], xv[E];
+            uint32_t f[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                v[e] = sell_val_flag<1>(dbs, u[e], dom);
+                xv[e] = sell_x(xb, u[e]);
+                f[e] = u[e] & 4u;
+            }
+            if (k < width) {
+                p += 32 * E;
+                S::load(p, u);
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const double2 w = f[e] ? tdom : make_double2(0.0, 0.0);
+                cmac(sr[e], si[e], v[e], xv[e]);
+                cmac(tr[e], ti[e], w, xv[e]);
+            }
+        }
+    }
+#else
     for (int k = 0; k < width; ++k) {
         uint32_t u[E];
         S::load(p, u);
@@ -636,6 +667,7 @@ __device__ __forceinline__ void sell_spmv_tdd(const uint32_t* __restrict__ ent, 
             cmac(tr[e], ti[e], w, xv);
         }
     }
+#endif
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         out0[e] = make_double2(sr[e], si[e]);
