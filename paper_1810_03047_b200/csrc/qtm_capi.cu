@@ -626,14 +626,9 @@ int build_sell(qtm_problem* p, const qtm_csr& g, int64_t n, int nt, int ncomp, s
             P.sell_tex = (unsigned long long)tex;
             p->sell_tex = tex;
         }
-        P.sell_td_dom_on = 0;
-        P.sell_td_dom = make_double2(0.0, 0.0);
-        if (tdd) {
-            P.sell_td = 1;
-            P.sell_td_dict = nullptr;
-            P.sell_td_ent = nullptr;
-            P.sell_td_dom_on = 1;
-            memcpy(&P.sell_td_dom, &tds[0]->values[0], 16);
+        if (tdd) {  // no tables: the term's one value in the pointers' storage
+            P.sell_td = -1;
+            memcpy(P.sell_td_dom, &tds[0]->values[0], 16);
         } else if (nt1) {
             double2* d_tdict = nullptr;
             uint16_t* d_tent = nullptr;

@@ -108,15 +108,23 @@ struct DevProblem {
     // the sell_td staged time-dependent terms, and sell_td_ent ([sell_td]
     // arrays of uint16 per slot, same slot layout) holds the byte offset of
     // G_k's value in sell_td_dict (offset 0 = 0.0); staged after the G0 entries
+    // sell_td == -1: a single staged term whose stored entries all hold ONE
+    // value (c4td: the modulated transverse field) needs no per-slot table at
+    // all -- bit 2 of the G0 entry says "G_1 has an entry here", its value is
+    // sell_td_dom (which shares the storage of the two unused table
+    // pointers), and G0's dominant value rides on bit 0 as in the
+    // time-independent kernels.  (No new fields: growing this struct moves
+    // the offsets of the kernel's second parameter, and with that alone the
+    // register allocation of the time-independent TMEM variant gained 112
+    // spill instructions and c4 ran 1.3 % slower.)
     int sell_td, sell_td_dict_n;
-    const double2* sell_td_dict;
-    const uint16_t* sell_td_ent;
-    // a single staged term whose stored entries all hold ONE value (c4td: the
-    // modulated transverse field): no per-slot table at all -- bit 2 of the
-    // G0 entry says "G_1 has an entry here", its value is sell_td_dom, and
-    // G0's dominant value rides on bit 0 as in the time-independent kernels
-    int sell_td_dom_on;
-    double2 sell_td_dom;
+    union {
+        struct {
+            const double2* sell_td_dict;
+            const uint16_t* sell_td_ent;
+        };
+        double sell_td_dom[2];
+    };
     // observables that are diagonal in the basis (number operators, sigma_z):
     // bit k of e_diag_mask set => dense values at e_diag[k * DP + i]
     unsigned e_diag_mask;
@@ -609,7 +617,7 @@ __device__ __forceinline__ void sell_spmv_td(const uint32_t* __restrict__ ent, c
 #define QTM_TDD_PF 0
 #endif
 // The same two products when G_1's stored entries all hold one value
-// (DevProblem::sell_td_dom_on): G_1's value per slot is `tdom` where bit 2 of
+// (DevProblem::sell_td == -1): G_1's value per slot is `tdom` where bit 2 of
 // the entry is set and an exact zero elsewhere -- the bits sell_spmv_td reads
 // from its tables -- and G0's dominant value comes from `dom` (bit 0).  Two
 // shared-memory loads per slot (entry, gathered x) plus the diagonal's value
@@ -1544,7 +1552,7 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
     if (P.sell_mode) {
         for (int i = tid; i < P.sell_dict_n; i += NT) s_dict[i] = P.sell_dict[i];
         for (int i = tid; i < P.sell_entries; i += NT) s_ent[i] = P.sell_ent[i];
-        if (TD && P.sell_td && !P.sell_td_dom_on) {
+        if (TD && P.sell_td > 0) {
             for (int i = tid; i < P.sell_td_dict_n; i += NT) s_tdict[i] = P.sell_td_dict[i];
             for (int i = tid; i < P.sell_td * P.sell_entries; i += NT) s_tent[i] = P.sell_td_ent[i];
         }
@@ -1559,10 +1567,11 @@ traj_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ RunPar
 #define GSPMV_T(xs, f, tt)                                                   \
     do {                                                                     \
         if constexpr (TD) {                                                  \
-            if (P.sell_td == 1) {                                            \
+            if (P.sell_td == 1 || P.sell_td == -1) {                         \
                 double2 g__[E];                                              \
-                if (P.sell_td_dom_on)                                        \
-                    sell_spmv_tdd<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f, g__, P.sell_dom, P.sell_td_dom); \
+                if (P.sell_td < 0)                                           \
+                    sell_spmv_tdd<NT, E>(s_ent, s_dict, goff, gwidth, (xs), f, g__, P.sell_dom, \
+                                         make_double2(P.sell_td_dom[0], P.sell_td_dom[1])); \
                 else                                                         \
                     sell_spmv_td<NT, E>(s_ent, s_dict, s_tent, s_tdict, goff, gwidth, (xs), f, g__); \
                 const double c__ = td_coef(P, 0, (tt));                      \
